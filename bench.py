@@ -1,0 +1,322 @@
+#!/usr/bin/env python3
+"""DEM step benchmark (BASELINE.json metric: particle-updates/s; force-kernel HBM % of peak).
+
+Workload at N=1: BASELINE.json configs[1] — 262,144 monodisperse spheres, dense random packing
+(SURVEY §8d generator G(262144, s=1.8, jit=0.2, mono, seed=1), dt=1e-5, g=0, no walls, K=16),
+fp64 (the reference's arithmetic). One "step" = one Simulation::step() (pipeline.cpp:366-378):
+integrate, bin, detect, force, history merge, reduce.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Timing: W untimed warm-up steps, then K steps each timed with CUDA events on the launching
+stream; before every timed step a 512 MiB buffer is overwritten to flush L2 (126 MB), outside
+the events. value = N_particles * K * world / max-over-ranks(sum of step times).
+e2e: the same metric through the C ABI with host buffers: per step the full particle state is
+uploaded from host memory (dem_set_particles), one step runs, and the state is read back
+(dem_get_particles); wall-clock per step.
+--impl reference: the reference's own CPU Simulation::step() (oracle/_ref, compiled from the
+reference sources) on this host with all cores, on the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_PARTICLES = 262144
+FLUSH_BYTES = 512 << 20
+METRIC = "particle-updates/sec"
+UNIT = "particle-updates/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def algorithmic_bytes(n, c, m):
+    """Compulsory bytes per launch of each kernel (d64); see DESIGN.md §4 for the derivation."""
+    return {
+        "k_phase_begin": 0,
+        "k_integrate_hash": 252 * n,
+        "k_scan_cells": 12 * m,
+        "k_scatter": 24 * n,
+        "k_reorder": 236 * n,
+        "k_detect": 40 * n + 4 * m + 8 * c,
+        "k_force": 112 * n + 113 * c,
+        "k_reduce": 72 * n + 53 * c,
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    smax = float(parts[2])
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        except FileNotFoundError:
+            pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def workload(seed=1):
+    import paper_1503_03553_b200 as dem
+    ps, dmax = dem.gen_packing(N_PARTICLES, s=1.8, jit=0.2, poly=False, seed=seed)
+    cfg = dem.packing_config(dmax)
+    return ps, cfg
+
+
+def cpu_reference_run(ps, cfg, steps, warmup, budget_s, threads=None):
+    """Reference Simulation::step() on host cores (oracle/_ref). Returns dict."""
+    from oracle.oracle import RefLib, RefSim
+    ref = RefLib()
+    if threads:
+        ref.set_threads(threads)
+    cores = ref.thread_count()
+    t0 = time.perf_counter()
+    sim = RefSim(ref, ps, cfg)  # priming pass untimed, pipeline.cpp:83
+    t_ctor = time.perf_counter() - t0
+    for _ in range(warmup):
+        sim.step()
+    done, t_total = 0, 0.0
+    while done < steps:
+        t1 = time.perf_counter()
+        sim.step()
+        t_total += time.perf_counter() - t1
+        done += 1
+        if t_total > budget_s:
+            break
+    value = len(ps.ids) * done / t_total
+    return {"value": value, "steps": done, "seconds": t_total, "cores": cores, "ctor_s": t_ctor}
+
+
+def run_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    ps, cfg = workload()
+    budget = float(os.environ.get("DEM_REF_BUDGET_S", "120"))
+    r = cpu_reference_run(ps, cfg, args.steps, min(args.warmup, 1), budget)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
+        "n_gpus": args.gpus, "steps": r["steps"], "warmup": min(args.warmup, 1),
+        "ms_per_step": 1e3 * r["seconds"] / r["steps"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "262,144 monodisperse spheres, dense random packing (configs[1])",
+                   "generator": "G(262144, s=1.8, jit=0.2, mono, seed=1)", "dt": 1e-5,
+                   "contact_capacity": 16, "parallelism": "cpu-threads"},
+        "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "reference",
+                         "sample": f"{r['steps']} full steps of the 262,144-particle workload "
+                                   f"({r['seconds']:.1f} s), DEMFORGE threads={r['cores']}"},
+        "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_b200(args):
+    world, rank, local = dist_env()
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    import paper_1503_03553_b200 as dem
+
+    # independent replicas of the workload, one per GPU (weak scaling; slab decomposition over
+    # NVLink is DESIGN.md §7 "next")
+    ps, cfg = workload(seed=1 + rank)
+    n = len(ps.ids)
+    sim = dem.Simulation(ps, cfg, device=local)
+    for _ in range(args.warmup):
+        sim.step()
+
+    # --- timed region: K steps, CUDA events per step on the launching stream ---
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        step_ms, m_last = sim.time_steps(args.steps, FLUSH_BYTES)
+    torch.cuda.synchronize()
+    barrier(world)
+    total_s = sum(step_ms) / 1e3
+    total_s_max = max_over_ranks(total_s, world)
+    value = n * args.steps * world / total_s_max
+    ms_per_step = 1e3 * total_s_max / args.steps
+
+    # --- per-kernel device times (events between kernels, same stream, L2 flushed) ---
+    prof = []
+    for _ in range(3):
+        prof.append(sim.profile_step(FLUSH_BYTES))
+    names = dem.device_kernel_names()
+    kms = {nm: statistics.median(p.device_kernel_ms[k] for p in prof) for k, nm in enumerate(names)}
+    c = prof[-1].contacts
+    nbytes = algorithmic_bytes(n, c, prof[-1].cells)
+    dom = max((k for k in kms if k != "k_phase_begin"), key=lambda k: kms[k])
+    peak, peak_kind = peaks()
+    force_ach = nbytes["k_force"] / (kms["k_force"] * 1e-3) / 1e9
+    dom_ach = nbytes[dom] / (kms[dom] * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r01_force_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom)
+        except Exception:
+            traffic = None
+
+    # --- e2e through the C ABI with host buffers ---
+    e2e_steps = max(3, min(args.steps, 10))
+    host = sim.particles()
+    t_e2e = []
+    for _ in range(e2e_steps):
+        t0 = time.perf_counter()
+        sim.set_particles(host)
+        sim.step()
+        host = sim.particles()
+        t_e2e.append(time.perf_counter() - t0)
+    e2e_s = max_over_ranks(sum(t_e2e), world)
+    e2e_value = n * e2e_steps * world / e2e_s
+    state_bytes = n * (4 + 24 * 3 + 8 + 8 + 4)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (SURVEY §8d generator, xorshift64*)",
+        "config": {"workload": "262,144 monodisperse spheres, dense random packing (configs[1])",
+                   "generator": "G(262144, s=1.8, jit=0.2, mono, seed=1+rank)", "dt": 1e-5,
+                   "contact_capacity": 16, "contacts_per_step": c, "cells": prof[-1].cells,
+                   "parallelism": f"replicas x{world}" if world > 1 else "single-gpu",
+                   "l2": "flushed before every timed step (512 MiB write), outside the events"},
+        "gpu_launches": sim.kernels_per_step() * args.steps,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": state_bytes,
+                "d2h_bytes_per_step": state_bytes,
+                "how": "dem_set_particles(host) + dem_step(1) + dem_get_particles(host), wall clock"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_ach, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": dom_ach / peak,
+                     "traffic": traffic, "algorithmic_bytes": nbytes[dom], "ms": kms[dom]},
+        "force_kernel": {"achieved": force_ach, "frac": force_ach / peak, "ms": kms["k_force"],
+                         "algorithmic_bytes": nbytes["k_force"]},
+        "kernel_ms": kms,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            budget = float(os.environ.get("DEM_CPU_BUDGET_S", "20"))
+            r = cpu_reference_run(ps, cfg, 1000, 0, budget)
+            line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": r["cores"],
+                                    "kind": "reference",
+                                    "sample": f"{r['steps']} full steps of the same 262,144-particle "
+                                              f"workload ({r['seconds']:.1f} s) through the reference "
+                                              f"Simulation::step() compiled from its sources"}
+        except Exception as e:  # noqa: BLE001
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(),
+                                    "kind": "reference", "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

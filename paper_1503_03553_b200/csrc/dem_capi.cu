@@ -1,0 +1,798 @@
+// dem_capi.cu — the C ABI (include/dem_b200.h): context lifetime, validation, host<->device
+// layout conversion, CUDA-graph step execution and error mapping.
+//
+// Host arithmetic that feeds the kernels (grid, per-material-pair tables) is compiled with
+// -ffp-contract=off so it rounds exactly as the reference does (core/CMakeLists.txt:32-37).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/dem_b200.h"
+#include "dem_internal.h"
+
+using namespace demb200;
+
+namespace {
+
+const char* kKernelNames[DEM_KERNEL_COUNT] = {
+    "Integrate", "CalcHash", "BitonicSort", "FindCellBoundsAndReorder", "ForceGravity",
+    "InitializeContactIDs", "Collide", "CollideRectangle", "CollideLine"};  // pipeline.cpp:16-29
+const char* kDeviceKernelNames[DEM_DEVICE_KERNEL_COUNT] = {
+    "k_phase_begin", "k_integrate_hash", "k_scan_cells", "k_scatter",
+    "k_reorder",     "k_detect",         "k_force",      "k_reduce"};
+
+}  // namespace
+
+struct dem_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+
+    // configuration
+    double dt = 0.0, gravity[3] = {0, 0, 0};
+    double domain_min[3] = {0, 0, 0}, domain_max[3] = {0, 0, 0};
+    std::vector<dem_material> materials;
+    std::vector<double> pair_rest;
+    std::vector<dem_rect_wall> rects;
+    std::vector<dem_line_wall> lines;
+    double grid_cell_size = 0.0;
+    int K = 16;
+    int collide_variant = 1;
+    dem_grid grid{};
+    uint64_t n = 0;
+    uint32_t M = 0;
+    size_t cap = 0;
+
+    // device memory
+    StateBuf state[2]{};
+    HistBuf hist[2]{};
+    double* ft = nullptr;
+    uint32_t *key = nullptr, *skey = nullptr, *loc = nullptr, *cnt = nullptr, *cstart = nullptr;
+    uint32_t *tmp_src = nullptr, *tmp_id = nullptr, *prev_slot = nullptr;
+    uint32_t *pair_i = nullptr, *pair_j = nullptr;
+    double* pft = nullptr;
+    uint8_t* pflag = nullptr;
+    unsigned long long *status_scan = nullptr, *status_det = nullptr;
+    uint32_t n_tiles_scan = 0, n_tiles_det = 0;
+    DevCtl* ctl = nullptr;
+    MatPairH* d_pairs = nullptr;
+    RectW* d_rects = nullptr;
+    LineW* d_lines = nullptr;
+    std::vector<void*> allocations;
+    uint64_t device_bytes = 0;
+
+    // execution state
+    uint64_t phase_count = 0;  // force phases executed (parity selects buffers)
+    int64_t step_index = 0;
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    void* flush_buf = nullptr;
+    size_t flush_bytes = 0;
+    DevCtl* h_ctl = nullptr;  // pinned readback
+    dem_error last_error{};
+};
+
+namespace {
+
+int set_error(dem_ctx* c, int code, int kernel, uint32_t slot, uint32_t id, int64_t step, const std::string& msg) {
+    if (c) {
+        c->last_error.code = code;
+        c->last_error.kernel = kernel;
+        c->last_error.particle_slot = slot;
+        c->last_error.particle_id = id;
+        c->last_error.step = step;
+        std::snprintf(c->last_error.message, sizeof(c->last_error.message), "%s", msg.c_str());
+    }
+    return code;
+}
+
+thread_local dem_error g_create_error{};
+
+#define CUDA_TRY(expr)                                                                   \
+    do {                                                                                 \
+        cudaError_t e_ = (expr);                                                         \
+        if (e_ != cudaSuccess) {                                                         \
+            return set_error(ctx, DEM_ERR_CUDA, -1, 0, 0, ctx ? ctx->step_index : 0,     \
+                             std::string("CUDA: ") + cudaGetErrorString(e_) + " at " #expr); \
+        }                                                                                \
+    } while (0)
+
+template <typename T>
+cudaError_t dalloc(dem_ctx* c, T** p, size_t count) {
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), bytes);
+    if (e == cudaSuccess) {
+        c->allocations.push_back(*p);
+        c->device_bytes += bytes;
+        e = cudaMemsetAsync(*p, 0, bytes, c->stream);
+    }
+    return e;
+}
+
+bool finite3(const double* p) { return std::isfinite(p[0]) && std::isfinite(p[1]) && std::isfinite(p[2]); }
+
+// SimConfig::validate (sim_config.cpp:10-60) for the fields the step consumes, and
+// ParticleSet::validate (particle_set.cpp:40-58).
+int validate(const dem_config* cfg, const dem_particles* p, std::string* why) {
+    auto fail = [&](const std::string& s) { *why = s; return DEM_ERR_CONFIG; };
+    if (!(cfg->dt > 0.0)) return fail("dt: must be > 0");
+    if (!finite3(cfg->gravity)) return fail("gravity: must be finite");
+    for (int a = 0; a < 3; ++a)
+        if (!(cfg->domain_max[a] - cfg->domain_min[a] > 0.0))
+            return fail("domain: min must be strictly below max on every axis");
+    if (cfg->material_count == 0 || !cfg->materials) return fail("no materials defined");
+    if (cfg->material_count > static_cast<uint32_t>(kMaxMaterials)) return fail("too many materials for the B200 tables (max 16)");
+    for (uint32_t k = 0; k < cfg->material_count; ++k) {
+        const dem_material& m = cfg->materials[k];
+        const std::string w = "material." + std::to_string(k) + ".";
+        if (!(m.poisson_ratio >= 0.0 && m.poisson_ratio < 0.5)) return fail(w + "poisson: must satisfy 0 <= sigma < 0.5");
+        if (!(m.shear_modulus > 0.0)) return fail(w + "shear_modulus: must be > 0");
+        if (!(m.youngs_modulus > 0.0)) return fail(w + "youngs_modulus: must be > 0");
+        if (!(m.restitution > 0.0 && m.restitution <= 1.0)) return fail(w + "restitution: must satisfy 0 < eps <= 1");
+        if (!(m.sliding_friction >= 0.0)) return fail(w + "mu_d: must be >= 0");
+    }
+    if (cfg->grid_cell_size < 0.0) return fail("grid.cell_size: must be > 0");
+    if (cfg->contact_capacity < 1) return fail("contacts.capacity: must be >= 1");
+    if (cfg->contact_capacity > 384) return fail("contacts.capacity: B200 build supports at most 384");
+    if (cfg->rect_wall_count + cfg->line_wall_count > static_cast<uint32_t>(kMaxWalls)) return fail("too many walls (max 64)");
+    for (uint32_t k = 0; k < cfg->rect_wall_count; ++k) {
+        const dem_rect_wall& w = cfg->rect_walls[k];
+        const std::string where = "wall.rect." + std::to_string(k);
+        const double lu = std::sqrt(w.edge_u[0] * w.edge_u[0] + w.edge_u[1] * w.edge_u[1] + w.edge_u[2] * w.edge_u[2]);
+        const double lv = std::sqrt(w.edge_v[0] * w.edge_v[0] + w.edge_v[1] * w.edge_v[1] + w.edge_v[2] * w.edge_v[2]);
+        if (!(lu > 0.0) || !(lv > 0.0)) return fail(where + ": degenerate rectangle (zero-length edge)");
+        const double d = w.edge_u[0] * w.edge_v[0] + w.edge_u[1] * w.edge_v[1] + w.edge_u[2] * w.edge_v[2];
+        if (std::abs(d) > 1e-9 * lu * lv) return fail(where + ": edge_u and edge_v must be orthogonal");
+        if (w.material_id >= cfg->material_count) return fail(where + ": bad material");
+    }
+    for (uint32_t k = 0; k < cfg->line_wall_count; ++k) {
+        const dem_line_wall& w = cfg->line_walls[k];
+        const std::string where = "wall.line." + std::to_string(k);
+        const double dx = w.b[0] - w.a[0], dy = w.b[1] - w.a[1], dz = w.b[2] - w.a[2];
+        if (!(std::sqrt(dx * dx + dy * dy + dz * dz) > 0.0)) return fail(where + ": zero-length segment");
+        if (w.material_id >= cfg->material_count) return fail(where + ": bad material");
+    }
+    if (p->count >= (1ull << 31)) return fail("particle count must be < 2^31");
+    for (uint64_t i = 0; i < p->count; ++i) {
+        if (!(p->radii[i] > 0.0)) return fail("particle " + std::to_string(p->ids[i]) + ": radius must be > 0");
+        if (!(p->masses[i] > 0.0)) return fail("particle " + std::to_string(p->ids[i]) + ": mass must be > 0");
+        if (!finite3(p->positions + 3 * i) || !finite3(p->velocities + 3 * i) || !finite3(p->angular_velocities + 3 * i))
+            return fail("particle " + std::to_string(p->ids[i]) + ": non-finite state");
+        if (p->material_ids[i] >= cfg->material_count) return fail("particle " + std::to_string(p->ids[i]) + ": bad material");
+    }
+    return DEM_OK;
+}
+
+// make_grid, grid.cpp:10-28
+int make_grid(const dem_config* cfg, double r_max, dem_grid* g, std::string* why) {
+    const double ex = cfg->domain_max[0] - cfg->domain_min[0];
+    const double ey = cfg->domain_max[1] - cfg->domain_min[1];
+    const double ez = cfg->domain_max[2] - cfg->domain_min[2];
+    if (!(ex > 0.0 && ey > 0.0 && ez > 0.0)) { *why = "domain box is degenerate (min must be strictly below max)"; return DEM_ERR_CONFIG; }
+    double h = cfg->grid_cell_size;
+    if (h <= 0.0) h = 2.0 * r_max * (1.0 + 1e-6);
+    if (!(h > 0.0)) { *why = "grid.cell_size must be positive"; return DEM_ERR_CONFIG; }
+    for (int a = 0; a < 3; ++a) g->origin[a] = cfg->domain_min[a];
+    g->cell_size = h;
+    g->nx = std::max(1, static_cast<int>(std::ceil(ex / h)));
+    g->ny = std::max(1, static_cast<int>(std::ceil(ey / h)));
+    g->nz = std::max(1, static_cast<int>(std::ceil(ez / h)));
+    const int64_t cells = static_cast<int64_t>(g->nx) * g->ny * g->nz;
+    if (cells > (int64_t{1} << 31)) { *why = "grid has more than 2^31 cells; increase grid.cell_size"; return DEM_ERR_CONFIG; }
+    if (cells >= (int64_t{1} << 31) - 1) { *why = "grid too large for 32-bit cell keys"; return DEM_ERR_CONFIG; }
+    return DEM_OK;
+}
+
+double restitution_alpha(double restitution) {  // contact_mechanics.cpp:7-12
+    if (restitution >= 1.0) return 0.0;
+    const double ln_eps = std::log(restitution);
+    constexpr double pi = 3.14159265358979323846;
+    return -2.0 * ln_eps / std::sqrt(pi * pi + ln_eps * ln_eps);
+}
+
+StepParams make_params(const dem_ctx* c, uint32_t flags) {
+    StepParams p{};
+    p.ox = c->grid.origin[0]; p.oy = c->grid.origin[1]; p.oz = c->grid.origin[2];
+    p.h = c->grid.cell_size;
+    p.inv_h = 1.0 / c->grid.cell_size;  // grid.cpp:32
+    p.nx = c->grid.nx; p.ny = c->grid.ny; p.nz = c->grid.nz;
+    p.M = c->M;
+    p.dt = c->dt;
+    p.gx = c->gravity[0]; p.gy = c->gravity[1]; p.gz = c->gravity[2];
+    p.n = static_cast<uint32_t>(c->n);
+    p.K = c->K;
+    p.nmat = static_cast<int>(c->materials.size());
+    p.nrect = static_cast<int>(c->rects.size());
+    p.nline = static_cast<int>(c->lines.size());
+    p.flags = flags;
+    p.pairs = c->d_pairs;
+    p.rects = c->d_rects;
+    p.lines = c->d_lines;
+    return p;
+}
+
+// Buffers of force phase number `phase` (1-based): state (phase-1)%2 -> phase%2.
+PhaseBufs make_bufs(const dem_ctx* c, uint64_t phase) {
+    PhaseBufs b{};
+    const int cur = static_cast<int>(phase & 1), prev = cur ^ 1;
+    b.src = c->state[prev];
+    b.dst = c->state[cur];
+    b.old_h = c->hist[prev];
+    b.cur_h = c->hist[cur];
+    b.ft = c->ft;
+    b.key = c->key; b.skey = c->skey; b.loc = c->loc; b.cnt = c->cnt; b.cstart = c->cstart;
+    b.tmp_src = c->tmp_src; b.tmp_id = c->tmp_id; b.prev_slot = c->prev_slot;
+    b.pair_i = c->pair_i; b.pair_j = c->pair_j; b.pft = c->pft; b.pflag = c->pflag;
+    b.status_scan = c->status_scan; b.status_det = c->status_det;
+    b.n_tiles_scan = c->n_tiles_scan; b.n_tiles_det = c->n_tiles_det;
+    b.cap = c->cap;
+    b.ctl = c->ctl;
+    return b;
+}
+
+// Enqueue one force phase; with `ev` (9 events) records an event after each kernel.
+void enqueue_phase(const dem_ctx* c, uint32_t flags, uint64_t phase, cudaEvent_t* ev) {
+    const StepParams p = make_params(c, flags);
+    const PhaseBufs b = make_bufs(c, phase);
+    cudaStream_t s = c->stream;
+    if (ev) cudaEventRecord(ev[0], s);
+    launch_phase_begin(b, s);
+    if (ev) cudaEventRecord(ev[1], s);
+    launch_integrate_hash(p, b, (flags & DEM_PHASE_INTEGRATE) != 0, s);
+    if (ev) cudaEventRecord(ev[2], s);
+    launch_scan_cells(p, b, s);
+    if (ev) cudaEventRecord(ev[3], s);
+    launch_scatter(p, b, s);
+    if (ev) cudaEventRecord(ev[4], s);
+    launch_reorder(p, b, s);
+    if (ev) cudaEventRecord(ev[5], s);
+    launch_detect(p, b, s);
+    if (ev) cudaEventRecord(ev[6], s);
+    launch_force(p, b, c->num_sms, s);
+    if (ev) cudaEventRecord(ev[7], s);
+    launch_reduce(p, b, s);
+    if (ev) cudaEventRecord(ev[8], s);
+}
+
+int build_graphs(dem_ctx* ctx) {
+    for (int par = 0; par < 2; ++par) {
+        if (ctx->graph[par]) { cudaGraphExecDestroy(ctx->graph[par]); ctx->graph[par] = nullptr; }
+        cudaGraph_t g;
+        CUDA_TRY(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        enqueue_phase(ctx, DEM_PHASE_STEP, static_cast<uint64_t>(par), nullptr);
+        CUDA_TRY(cudaStreamEndCapture(ctx->stream, &g));
+        CUDA_TRY(cudaGraphInstantiate(&ctx->graph[par], g, 0));
+        cudaGraphDestroy(g);
+    }
+    return DEM_OK;
+}
+
+// Reads the control block after a sync; maps a device error to last_error.
+int collect(dem_ctx* ctx, dem_step_metrics* m, uint64_t phase_before, int64_t step_before, bool is_step) {
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, ctx->stream));
+    uint32_t C = 0;
+    const int cur = static_cast<int>(ctx->phase_count & 1);
+    CUDA_TRY(cudaMemcpyAsync(&C, ctx->hist[cur].off + ctx->n, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    CUDA_TRY(cudaGetLastError());
+    const DevCtl& d = *ctx->h_ctl;
+    if (d.err_key != kNoError) {
+        const uint64_t fail_phase = d.err_phase;
+        ctx->phase_count = d.phase;  // phases after the failing one were halted
+        const int64_t done = static_cast<int64_t>(fail_phase - phase_before);
+        const int64_t fail_step = is_step ? step_before + done : ctx->step_index;
+        ctx->step_index = is_step ? fail_step : ctx->step_index;
+        const int kernel = static_cast<int>(d.err_key >> 56);
+        const uint32_t slot = static_cast<uint32_t>((d.err_key >> 8) & 0xffffffffull);
+        const int code = static_cast<int>(d.err_key & 0xff);
+        const uint32_t id = static_cast<uint32_t>(d.err_sid[kernel] & 0xffffffffull);
+        std::string what;
+        const char* kname = kKernelNames[kernel];
+        if (code == DEM_ERR_KERNEL) {
+            what = std::string(kname) + ": non-finite force on particle " + std::to_string(id);  // pipeline.cpp:35-38
+        } else if (code == DEM_ERR_CAPACITY) {
+            what = std::string(kname) + ": contact capacity exceeded for particle " + std::to_string(slot) +
+                   " (capacity " + std::to_string(ctx->K) + ")";  // error.hpp:30-42
+        } else {
+            kname = "Collide";  // geometry.cpp:32 tags every degenerate contact "Collide"
+            what = std::string(kname) + ": coincident centers: contact normal undefined";
+        }
+        set_error(ctx, code, kernel, slot, id, fail_step, what);
+        // reset the device error word so the context can be inspected / reused
+        DevCtl clean = d;
+        clean.err_key = kNoError;
+        for (auto& s : clean.err_sid) s = kNoError;
+        clean.halted = 0;
+        CUDA_TRY(cudaMemcpy(ctx->ctl, &clean, sizeof(DevCtl), cudaMemcpyHostToDevice));
+        return code;
+    }
+    if (m) {
+        m->step = ctx->step_index;
+        m->contacts = C;
+        m->pp_contact_events = static_cast<int64_t>(d.pp_events);
+        m->max_contacts_per_particle = static_cast<int32_t>(d.max_per);
+        m->clamps = static_cast<int64_t>(d.clamps);
+        double fm;
+        std::memcpy(&fm, &d.fric_bits, sizeof(double));
+        m->friction_max_ratio = fm;
+        m->capped_contacts = static_cast<int64_t>(d.capped);
+        m->cells = ctx->M;
+    }
+    return DEM_OK;
+}
+
+void free_ctx(dem_ctx* c) {
+    if (!c) return;
+    if (c->device >= 0) cudaSetDevice(c->device);
+    for (auto& g : c->graph) if (g) cudaGraphExecDestroy(g);
+    for (void* p : c->allocations) cudaFree(p);
+    if (c->flush_buf) cudaFree(c->flush_buf);
+    if (c->h_ctl) cudaFreeHost(c->h_ctl);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+int allocate(dem_ctx* ctx) {
+    const uint64_t n = ctx->n;
+    ctx->cap = static_cast<size_t>(n) * static_cast<size_t>(ctx->K);
+    ctx->n_tiles_scan = scan_tiles(ctx->M);
+    ctx->n_tiles_det = detect_tiles(static_cast<uint32_t>(n));
+    for (int b = 0; b < 2; ++b) {
+        CUDA_TRY(dalloc(ctx, &ctx->state[b].pos_r, n));
+        CUDA_TRY(dalloc(ctx, &ctx->state[b].vel_m, n));
+        CUDA_TRY(dalloc(ctx, &ctx->state[b].omg, n));
+        CUDA_TRY(dalloc(ctx, &ctx->state[b].idm, n));
+        CUDA_TRY(dalloc(ctx, &ctx->hist[b].off, n + 1));
+        CUDA_TRY(dalloc(ctx, &ctx->hist[b].key, ctx->cap));
+        CUDA_TRY(dalloc(ctx, &ctx->hist[b].dt, 3 * ctx->cap));
+    }
+    CUDA_TRY(dalloc(ctx, &ctx->ft, 6 * n));
+    CUDA_TRY(dalloc(ctx, &ctx->key, n));
+    CUDA_TRY(dalloc(ctx, &ctx->skey, n));
+    CUDA_TRY(dalloc(ctx, &ctx->loc, n));
+    CUDA_TRY(dalloc(ctx, &ctx->cnt, static_cast<size_t>(ctx->M) + 4));
+    CUDA_TRY(dalloc(ctx, &ctx->cstart, static_cast<size_t>(ctx->M) + 4));
+    CUDA_TRY(dalloc(ctx, &ctx->tmp_src, n));
+    CUDA_TRY(dalloc(ctx, &ctx->tmp_id, n));
+    CUDA_TRY(dalloc(ctx, &ctx->prev_slot, n));
+    CUDA_TRY(dalloc(ctx, &ctx->pair_i, ctx->cap));
+    CUDA_TRY(dalloc(ctx, &ctx->pair_j, ctx->cap));
+    CUDA_TRY(dalloc(ctx, &ctx->pft, 6 * ctx->cap));
+    CUDA_TRY(dalloc(ctx, &ctx->pflag, ctx->cap));
+    CUDA_TRY(dalloc(ctx, &ctx->status_scan, ctx->n_tiles_scan + 1));
+    CUDA_TRY(dalloc(ctx, &ctx->status_det, ctx->n_tiles_det + 1));
+    CUDA_TRY(dalloc(ctx, &ctx->ctl, 1));
+    CUDA_TRY(dalloc(ctx, &ctx->d_pairs, kMaxMaterials * kMaxMaterials));
+    CUDA_TRY(dalloc(ctx, &ctx->d_rects, kMaxWalls));
+    CUDA_TRY(dalloc(ctx, &ctx->d_lines, kMaxWalls));
+    CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_ctl), sizeof(DevCtl)));
+    return DEM_OK;
+}
+
+int upload_tables(dem_ctx* ctx) {
+    const size_t m = ctx->materials.size();
+    std::vector<MatPairH> tab(m * m);
+    for (size_t a = 0; a < m; ++a)
+        for (size_t b = 0; b < m; ++b) {
+            const dem_material& ma = ctx->materials[a];
+            const dem_material& mb = ctx->materials[b];
+            MatPairH& t = tab[a * m + b];
+            t.shear_sum = (2.0 - ma.poisson_ratio) / ma.shear_modulus + (2.0 - mb.poisson_ratio) / mb.shear_modulus;
+            t.young_sum = (2.0 - ma.poisson_ratio * ma.poisson_ratio) / ma.youngs_modulus +
+                          (2.0 - mb.poisson_ratio * mb.poisson_ratio) / mb.youngs_modulus;
+            double eps;
+            if (!ctx->pair_rest.empty()) {
+                eps = ctx->pair_rest[a * m + b];
+            } else {
+                const size_t lo = std::min(a, b), hi = std::max(a, b);  // materials.cpp:58-64
+                eps = std::sqrt(ctx->materials[lo].restitution * ctx->materials[hi].restitution);
+            }
+            t.alpha = restitution_alpha(eps);
+            t.mu = std::sqrt(ma.sliding_friction * mb.sliding_friction);  // materials.cpp:66-68
+        }
+    std::vector<RectW> rw(ctx->rects.size());
+    for (size_t k = 0; k < rw.size(); ++k) {
+        for (int a = 0; a < 3; ++a) {
+            rw[k].c[a] = ctx->rects[k].corner[a];
+            rw[k].u[a] = ctx->rects[k].edge_u[a];
+            rw[k].v[a] = ctx->rects[k].edge_v[a];
+        }
+        rw[k].mat = ctx->rects[k].material_id;
+    }
+    std::vector<LineW> lw(ctx->lines.size());
+    for (size_t k = 0; k < lw.size(); ++k) {
+        for (int a = 0; a < 3; ++a) { lw[k].a[a] = ctx->lines[k].a[a]; lw[k].b[a] = ctx->lines[k].b[a]; }
+        lw[k].mat = ctx->lines[k].material_id;
+    }
+    if (!tab.empty()) CUDA_TRY(cudaMemcpyAsync(ctx->d_pairs, tab.data(), tab.size() * sizeof(MatPairH), cudaMemcpyHostToDevice, ctx->stream));
+    if (!rw.empty()) CUDA_TRY(cudaMemcpyAsync(ctx->d_rects, rw.data(), rw.size() * sizeof(RectW), cudaMemcpyHostToDevice, ctx->stream));
+    if (!lw.empty()) CUDA_TRY(cudaMemcpyAsync(ctx->d_lines, lw.data(), lw.size() * sizeof(LineW), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return DEM_OK;
+}
+
+int upload_state(dem_ctx* ctx, const dem_particles* p, int buf) {
+    const uint64_t n = ctx->n;
+    std::vector<double4> pr(n), vm(n), om(n);
+    std::vector<uint2> idm(n);
+    for (uint64_t i = 0; i < n; ++i) {
+        pr[i] = make_double4(p->positions[3 * i], p->positions[3 * i + 1], p->positions[3 * i + 2], p->radii[i]);
+        vm[i] = make_double4(p->velocities[3 * i], p->velocities[3 * i + 1], p->velocities[3 * i + 2], p->masses[i]);
+        om[i] = make_double4(p->angular_velocities[3 * i], p->angular_velocities[3 * i + 1], p->angular_velocities[3 * i + 2], 0.0);
+        idm[i] = make_uint2(p->ids[i], p->material_ids[i]);
+    }
+    if (n) {
+        CUDA_TRY(cudaMemcpyAsync(ctx->state[buf].pos_r, pr.data(), n * sizeof(double4), cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(ctx->state[buf].vel_m, vm.data(), n * sizeof(double4), cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(ctx->state[buf].omg, om.data(), n * sizeof(double4), cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(ctx->state[buf].idm, idm.data(), n * sizeof(uint2), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return DEM_OK;
+}
+
+int run_phase(dem_ctx* ctx, uint32_t flags, dem_step_metrics* m, bool is_step) {
+    if (ctx->n == 0) {
+        if (is_step) ++ctx->step_index;
+        if (m) { std::memset(m, 0, sizeof(*m)); m->step = ctx->step_index; }
+        return DEM_OK;
+    }
+    const uint64_t pb = ctx->phase_count;
+    const int64_t sb = ctx->step_index;
+    ++ctx->phase_count;
+    if (is_step) ++ctx->step_index;
+    if (flags == DEM_PHASE_STEP && ctx->graph[ctx->phase_count & 1]) {
+        CUDA_TRY(cudaGraphLaunch(ctx->graph[ctx->phase_count & 1], ctx->stream));
+    } else {
+        enqueue_phase(ctx, flags, ctx->phase_count, nullptr);
+    }
+    return collect(ctx, m, pb, sb, is_step);
+}
+
+}  // namespace
+
+extern "C" {
+
+int dem_abi_version(void) { return DEM_B200_ABI_VERSION; }
+
+const char* dem_device_kernel_name(int k) {
+    return (k >= 0 && k < DEM_DEVICE_KERNEL_COUNT) ? kDeviceKernelNames[k] : "?";
+}
+
+int dem_create(const dem_config* cfg, const dem_particles* particles, int device, dem_ctx** out) {
+    dem_ctx* ctx = nullptr;
+    if (!cfg || !particles || !out) return DEM_ERR_ARGUMENT;
+    *out = nullptr;
+    std::string why;
+    int rc = validate(cfg, particles, &why);
+    if (rc != DEM_OK) {
+        std::snprintf(g_create_error.message, sizeof(g_create_error.message), "%s", why.c_str());
+        g_create_error.code = rc;
+        return rc;
+    }
+    double r_max = 0.0;
+    for (uint64_t i = 0; i < particles->count; ++i) r_max = std::max(r_max, particles->radii[i]);
+    dem_grid grid{};
+    rc = make_grid(cfg, r_max, &grid, &why);
+    if (rc != DEM_OK) {
+        std::snprintf(g_create_error.message, sizeof(g_create_error.message), "%s", why.c_str());
+        g_create_error.code = rc;
+        return rc;
+    }
+    ctx = new (std::nothrow) dem_ctx();
+    if (!ctx) return DEM_ERR_ARGUMENT;
+    ctx->device = device;
+    if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        std::snprintf(g_create_error.message, sizeof(g_create_error.message), "CUDA device %d unavailable", device);
+        g_create_error.code = DEM_ERR_CUDA;
+        free_ctx(ctx);
+        return DEM_ERR_CUDA;
+    }
+    cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+    init_device_attributes();
+    ctx->dt = cfg->dt;
+    for (int a = 0; a < 3; ++a) {
+        ctx->gravity[a] = cfg->gravity[a];
+        ctx->domain_min[a] = cfg->domain_min[a];
+        ctx->domain_max[a] = cfg->domain_max[a];
+    }
+    ctx->materials.assign(cfg->materials, cfg->materials + cfg->material_count);
+    if (cfg->pair_restitution)
+        ctx->pair_rest.assign(cfg->pair_restitution, cfg->pair_restitution + cfg->material_count * cfg->material_count);
+    if (cfg->rect_wall_count) ctx->rects.assign(cfg->rect_walls, cfg->rect_walls + cfg->rect_wall_count);
+    if (cfg->line_wall_count) ctx->lines.assign(cfg->line_walls, cfg->line_walls + cfg->line_wall_count);
+    ctx->grid_cell_size = cfg->grid_cell_size;
+    ctx->K = cfg->contact_capacity;
+    ctx->collide_variant = cfg->collide_variant;
+    ctx->grid = grid;
+    ctx->n = particles->count;
+    ctx->M = static_cast<uint32_t>(static_cast<int64_t>(grid.nx) * grid.ny * grid.nz);
+    rc = allocate(ctx);
+    if (rc == DEM_OK) rc = upload_tables(ctx);
+    if (rc == DEM_OK) {
+        DevCtl init{};
+        init.err_key = kNoError;
+        for (auto& s : init.err_sid) s = kNoError;
+        if (cudaMemcpy(ctx->ctl, &init, sizeof(DevCtl), cudaMemcpyHostToDevice) != cudaSuccess) rc = DEM_ERR_CUDA;
+    }
+    if (rc == DEM_OK) rc = upload_state(ctx, particles, 0);
+    if (rc == DEM_OK) rc = build_graphs(ctx);
+    // priming force pass, pipeline.cpp:83
+    if (rc == DEM_OK) rc = run_phase(ctx, DEM_PHASE_GRAVITY | DEM_PHASE_PP | DEM_PHASE_RECT | DEM_PHASE_LINE, nullptr, false);
+    if (rc != DEM_OK) {
+        g_create_error = ctx->last_error;
+        g_create_error.code = rc;
+        free_ctx(ctx);
+        return rc;
+    }
+    *out = ctx;
+    return DEM_OK;
+}
+
+int dem_clone(const dem_ctx* src, dem_ctx** out) {
+    if (!src || !out) return DEM_ERR_ARGUMENT;
+    dem_ctx* ctx = new (std::nothrow) dem_ctx();
+    if (!ctx) return DEM_ERR_ARGUMENT;
+    ctx->device = src->device;
+    cudaSetDevice(ctx->device);
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) { free_ctx(ctx); return DEM_ERR_CUDA; }
+    ctx->num_sms = src->num_sms;
+    init_device_attributes();
+    ctx->dt = src->dt;
+    std::memcpy(ctx->gravity, src->gravity, sizeof(ctx->gravity));
+    std::memcpy(ctx->domain_min, src->domain_min, sizeof(ctx->domain_min));
+    std::memcpy(ctx->domain_max, src->domain_max, sizeof(ctx->domain_max));
+    ctx->materials = src->materials; ctx->pair_rest = src->pair_rest;
+    ctx->rects = src->rects; ctx->lines = src->lines;
+    ctx->grid_cell_size = src->grid_cell_size; ctx->K = src->K; ctx->collide_variant = src->collide_variant;
+    ctx->grid = src->grid; ctx->n = src->n; ctx->M = src->M;
+    int rc = allocate(ctx);
+    if (rc == DEM_OK) {
+        // allocations were made in the same order with the same sizes: copy pairwise
+        size_t k = 0;
+        auto copy = [&](void* dst, const void* s, size_t bytes) {
+            if (rc == DEM_OK && cudaMemcpyAsync(dst, s, bytes, cudaMemcpyDeviceToDevice, ctx->stream) != cudaSuccess) rc = DEM_ERR_CUDA;
+        };
+        const uint64_t n = src->n;
+        for (int b = 0; b < 2; ++b) {
+            copy(ctx->state[b].pos_r, src->state[b].pos_r, n * sizeof(double4));
+            copy(ctx->state[b].vel_m, src->state[b].vel_m, n * sizeof(double4));
+            copy(ctx->state[b].omg, src->state[b].omg, n * sizeof(double4));
+            copy(ctx->state[b].idm, src->state[b].idm, n * sizeof(uint2));
+            copy(ctx->hist[b].off, src->hist[b].off, (n + 1) * sizeof(uint32_t));
+            copy(ctx->hist[b].key, src->hist[b].key, src->cap * sizeof(uint32_t));
+            copy(ctx->hist[b].dt, src->hist[b].dt, 3 * src->cap * sizeof(double));
+        }
+        copy(ctx->ft, src->ft, 6 * n * sizeof(double));
+        copy(ctx->skey, src->skey, n * sizeof(uint32_t));
+        copy(ctx->prev_slot, src->prev_slot, n * sizeof(uint32_t));
+        copy(ctx->pair_i, src->pair_i, src->cap * sizeof(uint32_t));
+        copy(ctx->pair_j, src->pair_j, src->cap * sizeof(uint32_t));
+        copy(ctx->ctl, src->ctl, sizeof(DevCtl));
+        copy(ctx->d_pairs, src->d_pairs, kMaxMaterials * kMaxMaterials * sizeof(MatPairH));
+        copy(ctx->d_rects, src->d_rects, kMaxWalls * sizeof(RectW));
+        copy(ctx->d_lines, src->d_lines, kMaxWalls * sizeof(LineW));
+        (void)k;
+        if (rc == DEM_OK && cudaStreamSynchronize(ctx->stream) != cudaSuccess) rc = DEM_ERR_CUDA;
+    }
+    ctx->phase_count = src->phase_count;
+    ctx->step_index = src->step_index;
+    ctx->last_error = src->last_error;
+    if (rc == DEM_OK) rc = build_graphs(ctx);
+    if (rc != DEM_OK) { free_ctx(ctx); return rc; }
+    *out = ctx;
+    return DEM_OK;
+}
+
+void dem_destroy(dem_ctx* ctx) { free_ctx(ctx); }
+
+int dem_step(dem_ctx* ctx, int nsteps, dem_step_metrics* last) {
+    if (!ctx || nsteps < 0) return DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    if (ctx->n == 0) {
+        ctx->step_index += nsteps;
+        if (last) { std::memset(last, 0, sizeof(*last)); last->step = ctx->step_index; }
+        return DEM_OK;
+    }
+    const uint64_t pb = ctx->phase_count;
+    const int64_t sb = ctx->step_index;
+    for (int k = 0; k < nsteps; ++k) {
+        ++ctx->phase_count;
+        ++ctx->step_index;
+        CUDA_TRY(cudaGraphLaunch(ctx->graph[ctx->phase_count & 1], ctx->stream));
+    }
+    return collect(ctx, last, pb, sb, true);
+}
+
+int dem_force_phase(dem_ctx* ctx, uint32_t flags, dem_step_metrics* m) {
+    if (!ctx || (flags & ~static_cast<uint32_t>(DEM_PHASE_STEP))) return DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    return run_phase(ctx, flags, m, flags == DEM_PHASE_STEP);
+}
+
+int dem_set_collide_variant(dem_ctx* ctx, int variant) {
+    if (!ctx || (variant != 0 && variant != 1)) return DEM_ERR_ARGUMENT;
+    ctx->collide_variant = variant;
+    return DEM_OK;
+}
+
+uint64_t dem_size(const dem_ctx* ctx) { return ctx ? ctx->n : 0; }
+int64_t dem_step_index(const dem_ctx* ctx) { return ctx ? ctx->step_index : 0; }
+uint64_t dem_device_bytes(const dem_ctx* ctx) { return ctx ? ctx->device_bytes : 0; }
+int dem_kernels_per_step(const dem_ctx*) { return DEM_DEVICE_KERNEL_COUNT; }
+
+int dem_get_particles(dem_ctx* ctx, dem_particles* out) {
+    if (!ctx || !out || out->count != ctx->n) return DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    const uint64_t n = ctx->n;
+    const StateBuf& s = ctx->state[ctx->phase_count & 1];
+    std::vector<double4> pr(n), vm(n), om(n);
+    std::vector<uint2> idm(n);
+    if (n) {
+        CUDA_TRY(cudaMemcpyAsync(pr.data(), s.pos_r, n * sizeof(double4), cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(vm.data(), s.vel_m, n * sizeof(double4), cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(om.data(), s.omg, n * sizeof(double4), cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(idm.data(), s.idm, n * sizeof(uint2), cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    }
+    for (uint64_t i = 0; i < n; ++i) {
+        if (out->positions) { out->positions[3 * i] = pr[i].x; out->positions[3 * i + 1] = pr[i].y; out->positions[3 * i + 2] = pr[i].z; }
+        if (out->radii) out->radii[i] = pr[i].w;
+        if (out->velocities) { out->velocities[3 * i] = vm[i].x; out->velocities[3 * i + 1] = vm[i].y; out->velocities[3 * i + 2] = vm[i].z; }
+        if (out->masses) out->masses[i] = vm[i].w;
+        if (out->angular_velocities) { out->angular_velocities[3 * i] = om[i].x; out->angular_velocities[3 * i + 1] = om[i].y; out->angular_velocities[3 * i + 2] = om[i].z; }
+        if (out->ids) out->ids[i] = idm[i].x;
+        if (out->material_ids) out->material_ids[i] = idm[i].y;
+    }
+    return DEM_OK;
+}
+
+int dem_set_particles(dem_ctx* ctx, const dem_particles* in) {
+    if (!ctx || !in || in->count != ctx->n) return DEM_ERR_ARGUMENT;
+    if (!in->ids || !in->positions || !in->velocities || !in->angular_velocities || !in->radii || !in->masses || !in->material_ids)
+        return DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    return upload_state(ctx, in, static_cast<int>(ctx->phase_count & 1));
+}
+
+int dem_get_forces(dem_ctx* ctx, double* force, double* torque) {
+    if (!ctx) return DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    const uint64_t n = ctx->n;
+    std::vector<double> ft(6 * n);
+    if (n) {
+        CUDA_TRY(cudaMemcpyAsync(ft.data(), ctx->ft, 6 * n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    }
+    for (uint64_t i = 0; i < n; ++i)
+        for (int a = 0; a < 3; ++a) {
+            if (force) force[3 * i + a] = ft[a * n + i];
+            if (torque) torque[3 * i + a] = ft[(3 + a) * n + i];
+        }
+    return DEM_OK;
+}
+
+int dem_set_forces(dem_ctx* ctx, const double* force, const double* torque) {
+    if (!ctx || !force || !torque) return DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    const uint64_t n = ctx->n;
+    std::vector<double> ft(6 * n);
+    for (uint64_t i = 0; i < n; ++i)
+        for (int a = 0; a < 3; ++a) { ft[a * n + i] = force[3 * i + a]; ft[(3 + a) * n + i] = torque[3 * i + a]; }
+    if (n) {
+        CUDA_TRY(cudaMemcpyAsync(ctx->ft, ft.data(), 6 * n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    }
+    return DEM_OK;
+}
+
+int dem_get_grid(const dem_ctx* ctx, dem_grid* out) {
+    if (!ctx || !out) return DEM_ERR_ARGUMENT;
+    *out = ctx->grid;
+    return DEM_OK;
+}
+
+int dem_get_order(dem_ctx* ctx, uint32_t* sorted_keys, uint32_t* permutation) {
+    if (!ctx) return DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    const uint64_t n = ctx->n;
+    if (n && sorted_keys) CUDA_TRY(cudaMemcpyAsync(sorted_keys, ctx->skey, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    if (n && permutation) CUDA_TRY(cudaMemcpyAsync(permutation, ctx->prev_slot, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    return DEM_OK;
+}
+
+int64_t dem_get_contacts(dem_ctx* ctx, uint32_t* owner_slot, int32_t* partner, double* delta_t, int64_t cap) {
+    if (!ctx) return -DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    const uint64_t n = ctx->n;
+    if (n == 0) return 0;
+    const HistBuf& h = ctx->hist[ctx->phase_count & 1];
+    std::vector<uint32_t> off(n + 1);
+    if (cudaMemcpy(off.data(), h.off, (n + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess) return -DEM_ERR_CUDA;
+    const int64_t C = off[n];
+    if (cap <= 0 || !owner_slot || !partner || !delta_t) return C;
+    const int64_t take = std::min<int64_t>(C, cap);
+    std::vector<uint32_t> pj(take);
+    std::vector<double> dt(3 * static_cast<size_t>(take));
+    if (take) {
+        if (cudaMemcpy(pj.data(), ctx->pair_j, take * sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess) return -DEM_ERR_CUDA;
+        for (int a = 0; a < 3; ++a)
+            if (cudaMemcpy(dt.data() + a * take, h.dt + a * ctx->cap, take * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+                return -DEM_ERR_CUDA;
+    }
+    for (uint64_t i = 0; i < n; ++i)
+        for (uint32_t q = off[i]; q < off[i + 1] && q < static_cast<uint64_t>(take); ++q) {
+            owner_slot[q] = static_cast<uint32_t>(i);
+            partner[q] = static_cast<int32_t>(pj[q]);  // wall codes ~w == -(w+1) (contact_table.hpp:35)
+            for (int a = 0; a < 3; ++a) delta_t[3 * q + a] = dt[a * take + q];
+        }
+    return C;
+}
+
+int dem_last_error(const dem_ctx* ctx, dem_error* out) {
+    if (!out) return DEM_ERR_ARGUMENT;
+    *out = ctx ? ctx->last_error : g_create_error;
+    return DEM_OK;
+}
+
+int dem_time_steps(dem_ctx* ctx, int nsteps, size_t flush_bytes, float* step_ms, dem_step_metrics* last) {
+    if (!ctx || nsteps < 0 || (nsteps && !step_ms)) return DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    if (flush_bytes && flush_bytes != ctx->flush_bytes) {
+        if (ctx->flush_buf) cudaFree(ctx->flush_buf);
+        ctx->flush_buf = nullptr;
+        CUDA_TRY(cudaMalloc(&ctx->flush_buf, flush_bytes));
+        ctx->flush_bytes = flush_bytes;
+    }
+    std::vector<cudaEvent_t> ev(2 * static_cast<size_t>(nsteps));
+    for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
+    const uint64_t pb = ctx->phase_count;
+    const int64_t sb = ctx->step_index;
+    for (int k = 0; k < nsteps; ++k) {
+        if (flush_bytes) launch_flush(ctx->flush_buf, flush_bytes, ctx->stream);
+        ++ctx->phase_count;
+        ++ctx->step_index;
+        CUDA_TRY(cudaEventRecord(ev[2 * k], ctx->stream));
+        CUDA_TRY(cudaGraphLaunch(ctx->graph[ctx->phase_count & 1], ctx->stream));
+        CUDA_TRY(cudaEventRecord(ev[2 * k + 1], ctx->stream));
+    }
+    int rc = collect(ctx, last, pb, sb, true);
+    for (int k = 0; k < nsteps; ++k) cudaEventElapsedTime(&step_ms[k], ev[2 * k], ev[2 * k + 1]);
+    for (auto& e : ev) cudaEventDestroy(e);
+    return rc;
+}
+
+int dem_profile_step(dem_ctx* ctx, size_t flush_bytes, dem_step_metrics* m) {
+    if (!ctx || !m) return DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    if (flush_bytes && flush_bytes != ctx->flush_bytes) {
+        if (ctx->flush_buf) cudaFree(ctx->flush_buf);
+        ctx->flush_buf = nullptr;
+        CUDA_TRY(cudaMalloc(&ctx->flush_buf, flush_bytes));
+        ctx->flush_bytes = flush_bytes;
+    }
+    cudaEvent_t ev[DEM_DEVICE_KERNEL_COUNT + 1];
+    for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
+    if (flush_bytes) launch_flush(ctx->flush_buf, flush_bytes, ctx->stream);
+    const uint64_t pb = ctx->phase_count;
+    const int64_t sb = ctx->step_index;
+    ++ctx->phase_count;
+    ++ctx->step_index;
+    enqueue_phase(ctx, DEM_PHASE_STEP, ctx->phase_count, ev);
+    int rc = collect(ctx, m, pb, sb, true);
+    for (int k = 0; k < DEM_DEVICE_KERNEL_COUNT; ++k) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+        m->device_kernel_ms[k] = ms;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    return rc;
+}
+
+}  // extern "C"

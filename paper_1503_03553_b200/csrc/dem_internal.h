@@ -1,0 +1,119 @@
+// dem_internal.h — device data layout and kernel launchers shared by dem_kernels.cu
+// (the sm_100a kernels) and dem_capi.cu (the C ABI / context / CUDA graphs).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace demb200 {
+
+constexpr int kMaxMaterials = 16;
+constexpr int kMaxWalls = 64;
+constexpr uint32_t kWallBit = 0x80000000u;  // partner codes >= this are walls: ~code = wall index
+constexpr unsigned long long kNoError = ~0ull;
+
+struct MatPairH {  // host mirror of MatPair (dem_math.cuh)
+    double shear_sum, young_sum, alpha, mu;
+};
+struct RectW {
+    double c[3], u[3], v[3];
+    uint32_t mat, pad;
+};
+struct LineW {
+    double a[3], b[3];
+    uint32_t mat, pad;
+};
+
+// Uniform per-phase parameters, passed by value.
+struct StepParams {
+    double ox, oy, oz;   // grid origin
+    double h, inv_h;     // cell size, 1.0 / h (grid.cpp:32)
+    int nx, ny, nz;
+    uint32_t M;          // nx*ny*nz
+    double dt;
+    double gx, gy, gz;
+    uint32_t n;          // particles
+    int K;               // contact capacity
+    int nmat;
+    int nrect, nline;
+    uint32_t flags;      // dem_phase_flags
+    const MatPairH* pairs;  // nmat*nmat, [owner][partner]
+    const RectW* rects;
+    const LineW* lines;
+};
+
+// Control block (device memory): error word, phase counter, per-phase metrics, tile counters.
+struct DevCtl {
+    unsigned long long err_key;                 // (kernel<<56)|(slot<<8)|code, atomicMin
+    unsigned long long err_sid[9];              // per kernel: (slot<<32)|stable id, atomicMin
+    unsigned long long err_phase;               // phase of the error
+    unsigned long long phase;                   // phases begun
+    unsigned int halted;                        // set by a phase begun after an error
+    unsigned int tile_ctr_scan;
+    unsigned int tile_ctr_detect;
+    unsigned int max_per;
+    unsigned long long clamps;
+    unsigned long long pp_events;
+    unsigned long long capped;
+    unsigned long long fric_bits;               // max of non-negative doubles as bits
+};
+
+// Structure-of-arrays particle state for one buffer (sorted slot order).
+struct StateBuf {
+    double4* pos_r;   // x, y, z, radius
+    double4* vel_m;   // vx, vy, vz, mass
+    double4* omg;     // wx, wy, wz, 0
+    uint2* idm;       // stable id, material id
+};
+
+struct HistBuf {
+    uint32_t* off;    // n+1 CSR offsets over slots
+    uint32_t* key;    // partner stable id, or wall code
+    double* dt;       // 3 * cap (SoA: x | y | z)
+};
+
+struct PhaseBufs {
+    StateBuf src, dst;       // reorder gathers src -> dst
+    HistBuf old_h, cur_h;    // history of previous phase / written this phase
+    double* ft;              // 6 * n (fx|fy|fz|tx|ty|tz), per slot
+    uint32_t* key;           // n: cell key per (pre-sort) slot, later sorted keys
+    uint32_t* skey;          // n: sorted keys (new slot order)
+    uint32_t* loc;           // n: arrival rank in cell
+    uint32_t* cnt;           // M: cell counts (kept zero between phases)
+    uint32_t* cstart;        // M+1
+    uint32_t* tmp_src;       // n
+    uint32_t* tmp_id;        // n
+    uint32_t* prev_slot;     // n
+    uint32_t* pair_i;        // cap
+    uint32_t* pair_j;        // cap
+    double* pft;             // 6 * cap, per-pair F, T
+    uint8_t* pflag;          // cap, bit0 matched history
+    unsigned long long* status_scan;
+    unsigned long long* status_det;
+    uint32_t n_tiles_scan, n_tiles_det;
+    size_t cap;              // pair capacity
+    DevCtl* ctl;
+};
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kDetectThreads = 128;
+
+inline uint32_t scan_tiles(uint32_t M) { return (M + kScanThreads * kScanItems - 1) / (kScanThreads * kScanItems); }
+inline uint32_t detect_tiles(uint32_t n) { return (n + kDetectThreads - 1) / kDetectThreads; }
+
+// Launchers (dem_kernels.cu). Each enqueues exactly one kernel on `s`.
+void launch_phase_begin(const PhaseBufs& b, cudaStream_t s);
+void launch_integrate_hash(const StepParams& p, const PhaseBufs& b, bool integrate, cudaStream_t s);
+void launch_scan_cells(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
+void launch_scatter(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
+void launch_reorder(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
+void launch_detect(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
+void launch_force(const StepParams& p, const PhaseBufs& b, int num_sms, cudaStream_t s);
+void launch_reduce(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
+void launch_flush(void* buf, size_t bytes, cudaStream_t s);
+cudaError_t init_device_attributes();
+
+}  // namespace demb200

@@ -61,8 +61,8 @@ typedef enum {
     DEM_DK_SCATTER,           /* counting-sort scatter (BitonicSort replacement)      */
     DEM_DK_REORDER,           /* canonical in-cell order + SoA gather (Reorder)       */
     DEM_DK_DETECT,            /* 27-cell detection -> compacted pair list (loop 1)    */
-    DEM_DK_FORCE,             /* Hertz-Mindlin per contact + history merge (loop 2)   */
-    DEM_DK_REDUCE,            /* per-particle deterministic sum + gravity + capacity  */
+    DEM_DK_FORCE_REDUCE,      /* Hertz-Mindlin per contact + history merge (loop 2)   */
+                              /* + per-particle deterministic sum, gravity, capacity  */
     DEM_DEVICE_KERNEL_COUNT
 } dem_device_kernel;
 

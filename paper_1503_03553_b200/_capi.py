@@ -12,7 +12,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdem_b200.so")
 
 DEM_KERNEL_COUNT = 9
-DEM_DEVICE_KERNEL_COUNT = 8
+DEM_DEVICE_KERNEL_COUNT = 7
 
 PHASE_INTEGRATE = 1
 PHASE_GRAVITY = 2

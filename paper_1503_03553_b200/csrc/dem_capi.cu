@@ -25,7 +25,7 @@ const char* kKernelNames[DEM_KERNEL_COUNT] = {
     "InitializeContactIDs", "Collide", "CollideRectangle", "CollideLine"};  // pipeline.cpp:16-29
 const char* kDeviceKernelNames[DEM_DEVICE_KERNEL_COUNT] = {
     "k_phase_begin", "k_integrate_hash", "k_scan_cells", "k_scatter",
-    "k_reorder",     "k_detect",         "k_force",      "k_reduce"};
+    "k_reorder",     "k_detect",         "k_force_reduce"};
 
 }  // namespace
 
@@ -56,8 +56,6 @@ struct dem_ctx {
     uint32_t *key = nullptr, *skey = nullptr, *loc = nullptr, *cnt = nullptr, *cstart = nullptr;
     uint32_t *tmp_src = nullptr, *tmp_id = nullptr, *prev_slot = nullptr;
     uint32_t *pair_i = nullptr, *pair_j = nullptr;
-    double* pft = nullptr;
-    uint8_t* pflag = nullptr;
     unsigned long long *status_scan = nullptr, *status_det = nullptr;
     uint32_t n_tiles_scan = 0, n_tiles_det = 0;
     DevCtl* ctl = nullptr;
@@ -227,7 +225,7 @@ PhaseBufs make_bufs(const dem_ctx* c, uint64_t phase) {
     b.ft = c->ft;
     b.key = c->key; b.skey = c->skey; b.loc = c->loc; b.cnt = c->cnt; b.cstart = c->cstart;
     b.tmp_src = c->tmp_src; b.tmp_id = c->tmp_id; b.prev_slot = c->prev_slot;
-    b.pair_i = c->pair_i; b.pair_j = c->pair_j; b.pft = c->pft; b.pflag = c->pflag;
+    b.pair_i = c->pair_i; b.pair_j = c->pair_j;
     b.status_scan = c->status_scan; b.status_det = c->status_det;
     b.n_tiles_scan = c->n_tiles_scan; b.n_tiles_det = c->n_tiles_det;
     b.cap = c->cap;
@@ -253,10 +251,8 @@ void enqueue_phase(const dem_ctx* c, uint32_t flags, uint64_t phase, cudaEvent_t
     if (ev) cudaEventRecord(ev[5], s);
     launch_detect(p, b, s);
     if (ev) cudaEventRecord(ev[6], s);
-    launch_force(p, b, c->num_sms, s);
+    launch_force_reduce(p, b, s);
     if (ev) cudaEventRecord(ev[7], s);
-    launch_reduce(p, b, s);
-    if (ev) cudaEventRecord(ev[8], s);
 }
 
 int build_graphs(dem_ctx* ctx) {
@@ -275,9 +271,6 @@ int build_graphs(dem_ctx* ctx) {
 // Reads the control block after a sync; maps a device error to last_error.
 int collect(dem_ctx* ctx, dem_step_metrics* m, uint64_t phase_before, int64_t step_before, bool is_step) {
     CUDA_TRY(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, ctx->stream));
-    uint32_t C = 0;
-    const int cur = static_cast<int>(ctx->phase_count & 1);
-    CUDA_TRY(cudaMemcpyAsync(&C, ctx->hist[cur].off + ctx->n, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     CUDA_TRY(cudaGetLastError());
     const DevCtl& d = *ctx->h_ctl;
@@ -313,7 +306,7 @@ int collect(dem_ctx* ctx, dem_step_metrics* m, uint64_t phase_before, int64_t st
     }
     if (m) {
         m->step = ctx->step_index;
-        m->contacts = C;
+        m->contacts = static_cast<int64_t>(d.contacts);
         m->pp_contact_events = static_cast<int64_t>(d.pp_events);
         m->max_contacts_per_particle = static_cast<int32_t>(d.max_per);
         m->clamps = static_cast<int64_t>(d.clamps);
@@ -339,15 +332,16 @@ void free_ctx(dem_ctx* c) {
 
 int allocate(dem_ctx* ctx) {
     const uint64_t n = ctx->n;
-    ctx->cap = static_cast<size_t>(n) * static_cast<size_t>(ctx->K);
     ctx->n_tiles_scan = scan_tiles(ctx->M);
     ctx->n_tiles_det = detect_tiles(static_cast<uint32_t>(n));
+    ctx->cap = static_cast<size_t>(ctx->n_tiles_det) * 32u * static_cast<size_t>(ctx->K);  // tile regions
     for (int b = 0; b < 2; ++b) {
         CUDA_TRY(dalloc(ctx, &ctx->state[b].pos_r, n));
         CUDA_TRY(dalloc(ctx, &ctx->state[b].vel_m, n));
         CUDA_TRY(dalloc(ctx, &ctx->state[b].omg, n));
         CUDA_TRY(dalloc(ctx, &ctx->state[b].idm, n));
-        CUDA_TRY(dalloc(ctx, &ctx->hist[b].off, n + 1));
+        CUDA_TRY(dalloc(ctx, &ctx->hist[b].pos, n));
+        CUDA_TRY(dalloc(ctx, &ctx->hist[b].cnt, n));
         CUDA_TRY(dalloc(ctx, &ctx->hist[b].key, ctx->cap));
         CUDA_TRY(dalloc(ctx, &ctx->hist[b].dt, 3 * ctx->cap));
     }
@@ -362,8 +356,6 @@ int allocate(dem_ctx* ctx) {
     CUDA_TRY(dalloc(ctx, &ctx->prev_slot, n));
     CUDA_TRY(dalloc(ctx, &ctx->pair_i, ctx->cap));
     CUDA_TRY(dalloc(ctx, &ctx->pair_j, ctx->cap));
-    CUDA_TRY(dalloc(ctx, &ctx->pft, 6 * ctx->cap));
-    CUDA_TRY(dalloc(ctx, &ctx->pflag, ctx->cap));
     CUDA_TRY(dalloc(ctx, &ctx->status_scan, ctx->n_tiles_scan + 1));
     CUDA_TRY(dalloc(ctx, &ctx->status_det, ctx->n_tiles_det + 1));
     CUDA_TRY(dalloc(ctx, &ctx->ctl, 1));
@@ -564,7 +556,8 @@ int dem_clone(const dem_ctx* src, dem_ctx** out) {
             copy(ctx->state[b].vel_m, src->state[b].vel_m, n * sizeof(double4));
             copy(ctx->state[b].omg, src->state[b].omg, n * sizeof(double4));
             copy(ctx->state[b].idm, src->state[b].idm, n * sizeof(uint2));
-            copy(ctx->hist[b].off, src->hist[b].off, (n + 1) * sizeof(uint32_t));
+            copy(ctx->hist[b].pos, src->hist[b].pos, n * sizeof(uint32_t));
+            copy(ctx->hist[b].cnt, src->hist[b].cnt, n * sizeof(uint32_t));
             copy(ctx->hist[b].key, src->hist[b].key, src->cap * sizeof(uint32_t));
             copy(ctx->hist[b].dt, src->hist[b].dt, 3 * src->cap * sizeof(double));
         }
@@ -713,24 +706,23 @@ int64_t dem_get_contacts(dem_ctx* ctx, uint32_t* owner_slot, int32_t* partner, d
     const uint64_t n = ctx->n;
     if (n == 0) return 0;
     const HistBuf& h = ctx->hist[ctx->phase_count & 1];
-    std::vector<uint32_t> off(n + 1);
-    if (cudaMemcpy(off.data(), h.off, (n + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess) return -DEM_ERR_CUDA;
-    const int64_t C = off[n];
+    std::vector<uint32_t> pos(n), cnt(n);
+    if (cudaMemcpy(pos.data(), h.pos, n * sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess) return -DEM_ERR_CUDA;
+    if (cudaMemcpy(cnt.data(), h.cnt, n * sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess) return -DEM_ERR_CUDA;
+    int64_t C = 0;
+    for (uint64_t i = 0; i < n; ++i) C += cnt[i];
     if (cap <= 0 || !owner_slot || !partner || !delta_t) return C;
-    const int64_t take = std::min<int64_t>(C, cap);
-    std::vector<uint32_t> pj(take);
-    std::vector<double> dt(3 * static_cast<size_t>(take));
-    if (take) {
-        if (cudaMemcpy(pj.data(), ctx->pair_j, take * sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess) return -DEM_ERR_CUDA;
-        for (int a = 0; a < 3; ++a)
-            if (cudaMemcpy(dt.data() + a * take, h.dt + a * ctx->cap, take * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
-                return -DEM_ERR_CUDA;
-    }
+    // tile regions -> dense list in slot order (per-owner accumulation order)
+    std::vector<uint32_t> pj(ctx->cap);
+    std::vector<double> dt(3 * ctx->cap);
+    if (cudaMemcpy(pj.data(), ctx->pair_j, ctx->cap * sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess) return -DEM_ERR_CUDA;
+    if (cudaMemcpy(dt.data(), h.dt, 3 * ctx->cap * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess) return -DEM_ERR_CUDA;
+    int64_t k = 0;
     for (uint64_t i = 0; i < n; ++i)
-        for (uint32_t q = off[i]; q < off[i + 1] && q < static_cast<uint64_t>(take); ++q) {
-            owner_slot[q] = static_cast<uint32_t>(i);
-            partner[q] = static_cast<int32_t>(pj[q]);  // wall codes ~w == -(w+1) (contact_table.hpp:35)
-            for (int a = 0; a < 3; ++a) delta_t[3 * q + a] = dt[a * take + q];
+        for (uint32_t q = pos[i]; q < pos[i] + cnt[i] && k < cap; ++q, ++k) {
+            owner_slot[k] = static_cast<uint32_t>(i);
+            partner[k] = static_cast<int32_t>(pj[q]);  // wall codes ~w == -(w+1) (contact_table.hpp:35)
+            for (int a = 0; a < 3; ++a) delta_t[3 * k + a] = dt[a * ctx->cap + q];
         }
     return C;
 }

@@ -58,6 +58,7 @@ struct DevCtl {
     unsigned long long pp_events;
     unsigned long long capped;
     unsigned long long fric_bits;               // max of non-negative doubles as bits
+    unsigned long long contacts;
 };
 
 // Structure-of-arrays particle state for one buffer (sorted slot order).
@@ -68,10 +69,14 @@ struct StateBuf {
     uint2* idm;       // stable id, material id
 };
 
+// Contacts of one force phase, tile-compacted: warp tile t (slots 32t..32t+31) owns the pair
+// slots [32 K t, 32 K (t+1)); inside it the contacts of its particles are dense, in slot order,
+// each particle's in accumulation order.
 struct HistBuf {
-    uint32_t* off;    // n+1 CSR offsets over slots
-    uint32_t* key;    // partner stable id, or wall code
-    double* dt;       // 3 * cap (SoA: x | y | z)
+    uint32_t* pos;    // n: first pair slot of particle i
+    uint32_t* cnt;    // n: number of contacts of particle i
+    uint32_t* key;    // cap: partner stable id, or wall code
+    double* dt;       // 3 * cap (SoA: x | y | z): tangential displacement after this phase
 };
 
 struct PhaseBufs {
@@ -88,8 +93,6 @@ struct PhaseBufs {
     uint32_t* prev_slot;     // n
     uint32_t* pair_i;        // cap
     uint32_t* pair_j;        // cap
-    double* pft;             // 6 * cap, per-pair F, T
-    uint8_t* pflag;          // cap, bit0 matched history
     unsigned long long* status_scan;
     unsigned long long* status_det;
     uint32_t n_tiles_scan, n_tiles_det;
@@ -99,10 +102,11 @@ struct PhaseBufs {
 
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
-constexpr int kDetectThreads = 128;
+constexpr int kDetectThreads = 256;  // 8 warps; a detection tile is one warp (32 slots)
 
 inline uint32_t scan_tiles(uint32_t M) { return (M + kScanThreads * kScanItems - 1) / (kScanThreads * kScanItems); }
-inline uint32_t detect_tiles(uint32_t n) { return (n + kDetectThreads - 1) / kDetectThreads; }
+// warp tiles launched (a multiple of the warps per block)
+inline uint32_t detect_tiles(uint32_t n) { return ((n + kDetectThreads - 1) / kDetectThreads) * (kDetectThreads / 32); }
 
 // Launchers (dem_kernels.cu). Each enqueues exactly one kernel on `s`.
 void launch_phase_begin(const PhaseBufs& b, cudaStream_t s);
@@ -111,8 +115,7 @@ void launch_scan_cells(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
 void launch_scatter(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
 void launch_reorder(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
 void launch_detect(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
-void launch_force(const StepParams& p, const PhaseBufs& b, int num_sms, cudaStream_t s);
-void launch_reduce(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
+void launch_force_reduce(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
 void launch_flush(void* buf, size_t bytes, cudaStream_t s);
 cudaError_t init_device_attributes();
 

@@ -281,6 +281,36 @@ class Oracle:
         return f, t, list(hout[:c]), (eo[:c].copy(), ep[:c].copy())
 
 
+HIST_DTYPE = np.dtype([("owner_id", "<u4"), ("partner_key", "<u4"), ("delta_t", "<f8", (3,))])
+assert HIST_DTYPE.itemsize == C.sizeof(orc_hist)
+
+
+def collide_arrays(orc: "Oracle", state, cfg, grid, owner_ids, partner_keys, delta_t):
+    """Vectorised Oracle.collide for large N: history in/out as numpy arrays.
+    Returns forces, torques, (owner_id, partner_key, delta_t) touched, (ev_owner, ev_partner)."""
+    n, keep, ptrs = _arr(state)
+    cc = CConfig(cfg)
+    hin = np.zeros(max(len(owner_ids), 1), HIST_DTYPE)
+    hin["owner_id"][:len(owner_ids)] = owner_ids
+    hin["partner_key"][:len(owner_ids)] = partner_keys
+    hin["delta_t"][:len(owner_ids)] = delta_t
+    cap = max(16, n * cfg.contact_capacity)
+    f = np.zeros((n, 3))
+    t = np.zeros((n, 3))
+    hout = np.zeros(cap, HIST_DTYPE)
+    eo = np.zeros(cap, np.uint32)
+    ep = np.zeros(cap, np.uint32)
+    c = orc.L.orc_collide(n, *ptrs, C.byref(cc.c), C.byref(grid),
+                          hin.ctypes.data_as(C.POINTER(orc_hist)), len(owner_ids),
+                          f.ctypes.data_as(PD), t.ctypes.data_as(PD),
+                          hout.ctypes.data_as(C.POINTER(orc_hist)), eo.ctypes.data_as(PU),
+                          ep.ctypes.data_as(PU), cap)
+    if c < 0:
+        raise OracleError(-c)
+    h = hout[:c]
+    return f, t, (h["owner_id"].copy(), h["partner_key"].copy(), h["delta_t"].copy()), (eo[:c].copy(), ep[:c].copy())
+
+
 class OracleSim:
     """Full-step restatement with canonical (cell, stable id) order (pipeline.cpp:31-378)."""
 

@@ -1,0 +1,414 @@
+// demb200/simulation.hpp — header-only C++ drop-in for the reference demforge::Simulation API
+// (/root/reference/proj/core/include/demforge/pipeline.hpp:62-136 and its value types), built on
+// the C ABI in dem_b200.h. Types live in namespace demb200 so a program can link this and the
+// reference (demforge::) side by side; `namespace demforge = demb200;` makes it a drop-in.
+//
+// Semantics kept from the reference:
+//  * the constructor validates, uploads and runs the priming force pass (pipeline.cpp:52-84);
+//  * step() runs Integrate then the force phase and returns StepMetrics (pipeline.cpp:366-378);
+//  * particles()/forces()/contact_table() return references into host mirrors that are synced
+//    lazily from the device; the non-const overloads mark the mirror dirty and the next kernel
+//    call uploads it (the reference lets callers mutate state between kernels, runner.cpp:131);
+//  * errors are rethrown as ConfigError / KernelError / CapacityError / DegenerateContactError
+//    with the reference kernel names (error.hpp:10-49, pipeline.cpp:16-29);
+//  * the class is copyable (a device-side clone, runner.cpp:261-270).
+#pragma once
+
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../dem_b200.h"
+
+namespace demb200 {
+
+// ---- vec3.hpp ----------------------------------------------------------------------------------
+struct Vec3 {
+    double x = 0.0, y = 0.0, z = 0.0;
+    constexpr Vec3() = default;
+    constexpr Vec3(double x_, double y_, double z_) : x(x_), y(y_), z(z_) {}
+    bool operator==(const Vec3&) const = default;
+};
+
+// ---- error.hpp ---------------------------------------------------------------------------------
+class ConfigError : public std::runtime_error {
+  public:
+    using std::runtime_error::runtime_error;
+};
+class KernelError : public std::runtime_error {
+  public:
+    KernelError(std::string kernel, const std::string& what)
+        : std::runtime_error(what), kernel_(std::move(kernel)) {}
+    const std::string& kernel() const { return kernel_; }
+
+  private:
+    std::string kernel_;
+};
+class CapacityError : public KernelError {
+  public:
+    CapacityError(std::string kernel, const std::string& what, std::uint32_t particle)
+        : KernelError(std::move(kernel), what), particle_(particle) {}
+    std::uint32_t particle() const { return particle_; }
+
+  private:
+    std::uint32_t particle_;
+};
+class DegenerateContactError : public KernelError {
+  public:
+    using KernelError::KernelError;
+};
+class DeviceError : public std::runtime_error {
+  public:
+    using std::runtime_error::runtime_error;
+};
+
+// ---- materials.hpp / geometry.hpp / sim_config.hpp --------------------------------------------
+struct MaterialParams {
+    double poisson_ratio = 0.3, shear_modulus = 4e5, youngs_modulus = 1e6, restitution = 0.9,
+           sliding_friction = 0.3;
+};
+
+class MaterialTable {
+  public:
+    std::uint32_t add(std::string name, const MaterialParams& p) {
+        for (const auto& n : names_)
+            if (n == name) throw ConfigError("material '" + name + "' defined twice");
+        names_.push_back(std::move(name));
+        mats_.push_back(p);
+        return static_cast<std::uint32_t>(mats_.size() - 1);
+    }
+    std::uint32_t index_of(const std::string& name) const {
+        for (std::size_t i = 0; i < names_.size(); ++i)
+            if (names_[i] == name) return static_cast<std::uint32_t>(i);
+        throw ConfigError("unknown material '" + name + "'");
+    }
+    const MaterialParams& params(std::uint32_t i) const { return mats_[i]; }
+    std::size_t size() const { return mats_.size(); }
+    void set_pair_restitution(std::uint32_t a, std::uint32_t b, double eps) {
+        if (a > b) std::swap(a, b);
+        for (auto& o : over_)
+            if (o.a == a && o.b == b) { o.eps = eps; return; }
+        over_.push_back({a, b, eps});
+    }
+    double pair_restitution(std::uint32_t a, std::uint32_t b) const {  // materials.cpp:58-64
+        if (a > b) std::swap(a, b);
+        for (const auto& o : over_)
+            if (o.a == a && o.b == b) return o.eps;
+        return std::sqrt(mats_[a].restitution * mats_[b].restitution);
+    }
+
+  private:
+    struct Override { std::uint32_t a, b; double eps; };
+    std::vector<std::string> names_;
+    std::vector<MaterialParams> mats_;
+    std::vector<Override> over_;
+};
+
+struct RectWall { Vec3 corner, edge_u, edge_v; std::uint32_t material_id = 0; };
+struct LineWall { Vec3 a, b; std::uint32_t material_id = 0; };
+enum class CollideVariant { baseline, two_phase };
+
+struct SimConfig {
+    double dt = 0.0;
+    Vec3 gravity{0.0, 0.0, -9.81};
+    Vec3 domain_min, domain_max;
+    MaterialTable materials;
+    std::vector<RectWall> rect_walls;
+    std::vector<LineWall> line_walls;
+    double grid_cell_size = 0.0;
+    int contact_capacity = 16;
+    CollideVariant collide_variant = CollideVariant::two_phase;
+};
+
+// ---- particle_set.hpp --------------------------------------------------------------------------
+struct ParticleSet {
+    std::vector<std::uint32_t> ids;
+    std::vector<Vec3> positions, velocities, angular_velocities;
+    std::vector<double> radii, masses;
+    std::vector<std::uint32_t> material_ids;
+    std::size_t size() const { return positions.size(); }
+    void push_back(std::uint32_t id, const Vec3& p, const Vec3& v, const Vec3& w, double r, double m,
+                   std::uint32_t mat) {
+        ids.push_back(id); positions.push_back(p); velocities.push_back(v);
+        angular_velocities.push_back(w); radii.push_back(r); masses.push_back(m); material_ids.push_back(mat);
+    }
+    bool operator==(const ParticleSet&) const = default;
+};
+
+struct ForceAccumulator {
+    std::vector<Vec3> force, torque;
+    bool operator==(const ForceAccumulator&) const = default;
+};
+
+// ---- contact_table.hpp (read API) ----------------------------------------------------------------
+struct ContactSlot {
+    std::int32_t partner = INT32_MIN;
+    bool touched = false;
+    Vec3 delta_t{};
+    bool empty() const { return partner == INT32_MIN; }
+};
+
+class ContactTable {
+  public:
+    ContactTable() = default;
+    ContactTable(std::uint32_t n, int capacity) : n_(n), cap_(capacity), slots_(std::size_t(n) * capacity) {}
+    static std::int32_t wall_id(int w) { return -(w + 1); }
+    static bool is_wall(std::int32_t p) { return p < 0; }
+    std::uint32_t particle_count() const { return n_; }
+    int capacity() const { return cap_; }
+    const ContactSlot* row(std::uint32_t p) const { return slots_.data() + std::size_t(p) * cap_; }
+    ContactSlot* row(std::uint32_t p) { return slots_.data() + std::size_t(p) * cap_; }
+    int live_count(std::uint32_t p) const {
+        int k = 0;
+        for (int s = 0; s < cap_; ++s) k += row(p)[s].empty() ? 0 : 1;
+        return k;
+    }
+    std::int64_t total_live() const {
+        std::int64_t k = 0;
+        for (const auto& s : slots_) k += s.empty() ? 0 : 1;
+        return k;
+    }
+    const ContactSlot* find(std::uint32_t p, std::int32_t partner) const {
+        for (int s = 0; s < cap_; ++s)
+            if (!row(p)[s].empty() && row(p)[s].partner == partner) return &row(p)[s];
+        return nullptr;
+    }
+
+  private:
+    std::uint32_t n_ = 0;
+    int cap_ = 0;
+    std::vector<ContactSlot> slots_;
+};
+
+struct UniformGrid {
+    Vec3 origin;
+    double cell_size = 0.0;
+    int nx = 1, ny = 1, nz = 1;
+    std::int64_t cell_count() const { return std::int64_t(nx) * ny * nz; }
+};
+
+// ---- pipeline.hpp ------------------------------------------------------------------------------
+struct StepMetrics {
+    std::int64_t step = 0, contacts = 0, pp_contact_events = 0;
+    int max_contacts_per_particle = 0;
+    std::int64_t clamps = 0;
+    double friction_max_ratio = 0.0;
+    std::int64_t capped_contacts = 0;
+};
+
+class Simulation {
+  public:
+    Simulation(ParticleSet initial, SimConfig config, int device = 0) : cfg_(std::move(config)) {
+        build_c_config();
+        dem_particles p = view(initial);
+        dem_ctx* c = nullptr;
+        const int rc = dem_create(&ccfg_, &p, device, &c);
+        if (rc != DEM_OK) rethrow(nullptr, rc);
+        ctx_.reset(c);
+        state_ = std::move(initial);
+        state_fresh_ = false;
+    }
+
+    Simulation(const Simulation& o) : cfg_(o.cfg_) {
+        o.flush();
+        build_c_config();
+        dem_ctx* c = nullptr;
+        const int rc = dem_clone(o.ctx_.get(), &c);
+        if (rc != DEM_OK) rethrow(o.ctx_.get(), rc);
+        ctx_.reset(c);
+    }
+    Simulation& operator=(const Simulation& o) {
+        if (this != &o) { Simulation t(o); *this = std::move(t); }
+        return *this;
+    }
+    Simulation(Simulation&&) = default;
+    Simulation& operator=(Simulation&&) = default;
+
+    StepMetrics step() { return run([&](dem_step_metrics* m) { return dem_step(ctx_.get(), 1, m); }, true); }
+    void set_record_traces(bool on) { record_traces_ = on; }
+    void set_collide_variant(CollideVariant v) {
+        cfg_.collide_variant = v;
+        check(dem_set_collide_variant(ctx_.get(), v == CollideVariant::two_phase ? 1 : 0));
+    }
+    /// advance_to_collide + kernel_collide (tests/test_pipeline.cpp:69-76): pp only, no gravity.
+    StepMetrics advance_and_collide() {
+        return run([&](dem_step_metrics* m) { return dem_force_phase(ctx_.get(), DEM_PHASE_INTEGRATE | DEM_PHASE_PP, m); }, false);
+    }
+    StepMetrics force_phase(std::uint32_t flags) {
+        return run([&](dem_step_metrics* m) { return dem_force_phase(ctx_.get(), flags, m); }, false);
+    }
+
+    const SimConfig& config() const { return cfg_; }
+    UniformGrid grid() const {
+        dem_grid g{};
+        dem_get_grid(ctx_.get(), &g);
+        return UniformGrid{Vec3{g.origin[0], g.origin[1], g.origin[2]}, g.cell_size, g.nx, g.ny, g.nz};
+    }
+    const ParticleSet& particles() const { sync_state(); return state_; }
+    ParticleSet& particles() { sync_state(); state_dirty_ = true; return state_; }
+    const ForceAccumulator& forces() const { sync_forces(); return forces_; }
+    ForceAccumulator& forces() { sync_forces(); forces_dirty_ = true; return forces_; }
+    const ContactTable& contact_table() const { sync_table(); return table_; }
+    std::int64_t step_index() const { return dem_step_index(ctx_.get()); }
+    std::int64_t last_clamp_count() const { return last_.clamps; }
+    double mean_coordination() const {
+        const auto n = dem_size(ctx_.get());
+        return n ? double(last_.pp_contact_events) / double(n) : 0.0;
+    }
+
+  private:
+    struct CtxDeleter { void operator()(dem_ctx* c) const { dem_destroy(c); } };
+
+    template <typename F>
+    StepMetrics run(F&& fn, bool) {
+        flush();
+        dem_step_metrics m{};
+        const int rc = fn(&m);
+        state_fresh_ = forces_fresh_ = table_fresh_ = false;
+        if (rc != DEM_OK) rethrow(ctx_.get(), rc);
+        last_ = StepMetrics{m.step, m.contacts, m.pp_contact_events, m.max_contacts_per_particle,
+                            m.clamps, m.friction_max_ratio, m.capped_contacts};
+        return last_;
+    }
+
+    void flush() const {
+        auto* self = const_cast<Simulation*>(this);
+        if (state_dirty_) {
+            dem_particles p = view(self->state_);
+            self->check(dem_set_particles(ctx_.get(), &p));
+            self->state_dirty_ = false;
+        }
+        if (forces_dirty_) {
+            self->check(dem_set_forces(ctx_.get(), &self->forces_.force[0].x, &self->forces_.torque[0].x));
+            self->forces_dirty_ = false;
+        }
+    }
+
+    void sync_state() const {
+        if (state_fresh_ || state_dirty_) return;
+        auto* self = const_cast<Simulation*>(this);
+        const auto n = dem_size(ctx_.get());
+        ParticleSet& s = self->state_;
+        s.ids.resize(n); s.positions.resize(n); s.velocities.resize(n); s.angular_velocities.resize(n);
+        s.radii.resize(n); s.masses.resize(n); s.material_ids.resize(n);
+        dem_particles p = view(s);
+        self->check(dem_get_particles(ctx_.get(), &p));
+        self->state_fresh_ = true;
+    }
+    void sync_forces() const {
+        if (forces_fresh_ || forces_dirty_) return;
+        auto* self = const_cast<Simulation*>(this);
+        const auto n = dem_size(ctx_.get());
+        self->forces_.force.resize(n);
+        self->forces_.torque.resize(n);
+        self->check(dem_get_forces(ctx_.get(), &self->forces_.force[0].x, &self->forces_.torque[0].x));
+        self->forces_fresh_ = true;
+    }
+    void sync_table() const {
+        if (table_fresh_) return;
+        auto* self = const_cast<Simulation*>(this);
+        const auto n = static_cast<std::uint32_t>(dem_size(ctx_.get()));
+        const std::int64_t c = dem_get_contacts(ctx_.get(), nullptr, nullptr, nullptr, 0);
+        std::vector<std::uint32_t> o(c);
+        std::vector<std::int32_t> p(c);
+        std::vector<double> d(3 * c);
+        dem_get_contacts(ctx_.get(), o.data(), p.data(), d.data(), c);
+        self->table_ = ContactTable(n, cfg_.contact_capacity);
+        std::vector<int> fill(n, 0);
+        for (std::int64_t k = 0; k < c; ++k) {
+            ContactSlot& s = self->table_.row(o[k])[fill[o[k]]++];
+            s.partner = p[k];
+            s.touched = true;
+            s.delta_t = Vec3{d[3 * k], d[3 * k + 1], d[3 * k + 2]};
+        }
+        self->table_fresh_ = true;
+    }
+
+    static dem_particles view(ParticleSet& s) {
+        dem_particles p{};
+        p.count = s.size();
+        p.ids = s.ids.data();
+        p.positions = &s.positions[0].x;
+        p.velocities = &s.velocities[0].x;
+        p.angular_velocities = &s.angular_velocities[0].x;
+        p.radii = s.radii.data();
+        p.masses = s.masses.data();
+        p.material_ids = s.material_ids.data();
+        return p;
+    }
+
+    void build_c_config() {
+        const auto m = cfg_.materials.size();
+        mats_.resize(m);
+        pair_.resize(m * m);
+        for (std::size_t k = 0; k < m; ++k) {
+            const auto& q = cfg_.materials.params(std::uint32_t(k));
+            mats_[k] = dem_material{q.poisson_ratio, q.shear_modulus, q.youngs_modulus, q.restitution, q.sliding_friction};
+        }
+        for (std::size_t a = 0; a < m; ++a)
+            for (std::size_t b = 0; b < m; ++b) pair_[a * m + b] = cfg_.materials.pair_restitution(std::uint32_t(a), std::uint32_t(b));
+        rects_.clear();
+        for (const auto& w : cfg_.rect_walls)
+            rects_.push_back(dem_rect_wall{{w.corner.x, w.corner.y, w.corner.z}, {w.edge_u.x, w.edge_u.y, w.edge_u.z},
+                                           {w.edge_v.x, w.edge_v.y, w.edge_v.z}, w.material_id});
+        lines_.clear();
+        for (const auto& w : cfg_.line_walls)
+            lines_.push_back(dem_line_wall{{w.a.x, w.a.y, w.a.z}, {w.b.x, w.b.y, w.b.z}, w.material_id});
+        ccfg_ = dem_config{};
+        ccfg_.dt = cfg_.dt;
+        ccfg_.gravity[0] = cfg_.gravity.x; ccfg_.gravity[1] = cfg_.gravity.y; ccfg_.gravity[2] = cfg_.gravity.z;
+        ccfg_.domain_min[0] = cfg_.domain_min.x; ccfg_.domain_min[1] = cfg_.domain_min.y; ccfg_.domain_min[2] = cfg_.domain_min.z;
+        ccfg_.domain_max[0] = cfg_.domain_max.x; ccfg_.domain_max[1] = cfg_.domain_max.y; ccfg_.domain_max[2] = cfg_.domain_max.z;
+        ccfg_.material_count = std::uint32_t(m);
+        ccfg_.materials = mats_.data();
+        ccfg_.pair_restitution = pair_.data();
+        ccfg_.rect_wall_count = std::uint32_t(rects_.size());
+        ccfg_.rect_walls = rects_.data();
+        ccfg_.line_wall_count = std::uint32_t(lines_.size());
+        ccfg_.line_walls = lines_.data();
+        ccfg_.grid_cell_size = cfg_.grid_cell_size;
+        ccfg_.contact_capacity = cfg_.contact_capacity;
+        ccfg_.collide_variant = cfg_.collide_variant == CollideVariant::two_phase ? 1 : 0;
+    }
+
+    void check(int rc) const { if (rc != DEM_OK) rethrow(ctx_.get(), rc); }
+
+    [[noreturn]] static void rethrow(const dem_ctx* c, int rc) {
+        dem_error e{};
+        dem_last_error(c, &e);
+        static const char* names[] = {"Integrate", "CalcHash", "BitonicSort", "FindCellBoundsAndReorder",
+                                      "ForceGravity", "InitializeContactIDs", "Collide", "CollideRectangle",
+                                      "CollideLine"};
+        const std::string kernel = (e.kernel >= 0 && e.kernel < DEM_KERNEL_COUNT) ? names[e.kernel] : "?";
+        switch (rc) {
+            case DEM_ERR_CONFIG: throw ConfigError(e.message);
+            case DEM_ERR_CAPACITY: throw CapacityError(kernel, e.message, e.particle_slot);
+            case DEM_ERR_DEGENERATE: throw DegenerateContactError("Collide", e.message);
+            case DEM_ERR_KERNEL: throw KernelError(kernel, e.message);
+            case DEM_ERR_ARGUMENT: throw std::invalid_argument(e.message);
+            default: throw DeviceError(e.message);
+        }
+    }
+
+    SimConfig cfg_;
+    dem_config ccfg_{};
+    std::vector<dem_material> mats_;
+    std::vector<double> pair_;
+    std::vector<dem_rect_wall> rects_;
+    std::vector<dem_line_wall> lines_;
+    std::unique_ptr<dem_ctx, CtxDeleter> ctx_;
+    mutable ParticleSet state_;
+    mutable ForceAccumulator forces_;
+    mutable ContactTable table_;
+    mutable bool state_fresh_ = false, forces_fresh_ = false, table_fresh_ = false;
+    mutable bool state_dirty_ = false, forces_dirty_ = false;
+    StepMetrics last_;
+    bool record_traces_ = false;
+};
+
+}  // namespace demb200

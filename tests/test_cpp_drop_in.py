@@ -1,0 +1,19 @@
+"""GPU: the C++ drop-in header (include/demb200/simulation.hpp) driven side by side with the
+reference demforge::Simulation in one C++ program (tests/cpp/drop_in_test.cpp)."""
+import os
+import subprocess
+
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+BIN = os.path.join(HERE, "cpp", "drop_in_test")
+
+
+@pytest.mark.gpu
+def test_cpp_drop_in_side_by_side(cuda):
+    if not os.path.exists(BIN):
+        pytest.skip("tests/cpp/drop_in_test not built (needs the reference headers at build time)")
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=300)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "PASSED" in r.stdout

@@ -239,7 +239,7 @@ def run_b200(args):
     force_ach = nbytes["k_force_reduce"] / (kms["k_force_reduce"] * 1e-3) / 1e9
     dom_ach = nbytes[dom] / (kms[dom] * 1e-3) / 1e9
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r01_force_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
     if os.path.exists(tpath):
         try:
             traffic = json.load(open(tpath)).get(dom)

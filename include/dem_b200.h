@@ -225,6 +225,30 @@ const char* dem_device_kernel_name(int k);
 /* Bytes of device memory the context holds. */
 uint64_t dem_device_bytes(const dem_ctx* ctx);
 
+/* ---- slab domain decomposition (multi-GPU; no reference counterpart:
+ * the reference is single-process) ----
+ * A slab context owns the particles whose global cell plane z is in [z_lo, z_hi). Each step the
+ * host runs, per rank:
+ *   dem_slab_migrate(integrate=1) -> exchange migrant records with the z-neighbours ->
+ *   dem_slab_import -> dem_slab_halo -> exchange ghost records -> dem_slab_ghosts ->
+ *   dem_slab_force(DEM_PHASE_STEP)
+ * (the constructor-equivalent priming pass is the same with integrate=0 and flags
+ * GRAVITY|PP|RECT|LINE). Record buffers are DEVICE pointers owned by the caller (e.g. torch
+ * tensors exchanged with NCCL); record sizes come from dem_slab_record_bytes. Results are
+ * bitwise identical to a single-GPU context because the in-cell order is canonical.
+ * config->grid_cell_size must be the global cell size (2 r_max (1 + 1e-6) over all ranks). */
+int dem_create_slab(const dem_config* config, const dem_particles* owned, int device, int32_t z_lo,
+                    int32_t z_hi, uint64_t capacity, dem_ctx** out);
+int dem_slab_record_bytes(const dem_ctx* ctx, uint64_t* migrant_bytes, uint64_t* ghost_bytes);
+uint64_t dem_slab_owned(const dem_ctx* ctx);
+int dem_slab_migrate(dem_ctx* ctx, int integrate, void* send_lo, void* send_hi, uint64_t cap_records,
+                     uint64_t* n_lo, uint64_t* n_hi);
+int dem_slab_import(dem_ctx* ctx, const void* recs_lo, uint64_t n_lo, const void* recs_hi, uint64_t n_hi);
+int dem_slab_halo(dem_ctx* ctx, void* send_lo, void* send_hi, uint64_t cap_records, uint64_t* n_lo,
+                  uint64_t* n_hi);
+int dem_slab_ghosts(dem_ctx* ctx, const void* recs_lo, uint64_t n_lo, const void* recs_hi, uint64_t n_hi);
+int dem_slab_force(dem_ctx* ctx, uint32_t flags, dem_step_metrics* metrics);
+
 #ifdef __cplusplus
 }
 #endif

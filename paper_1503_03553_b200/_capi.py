@@ -106,6 +106,17 @@ SIGNATURES = [
     ("dem_device_bytes", C.c_uint64, [_P]),
     ("dem_gen_packing", C.c_int, [C.c_uint64, C.c_double, C.c_double, C.c_int, C.c_uint64,
                                   C.c_double, C.POINTER(dem_particles), C.POINTER(C.c_double)]),
+    # slab decomposition
+    ("dem_create_slab", C.c_int, [C.POINTER(dem_config), C.POINTER(dem_particles), C.c_int, C.c_int32,
+                                  C.c_int32, C.c_uint64, C.POINTER(_P)]),
+    ("dem_slab_record_bytes", C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    ("dem_slab_owned", C.c_uint64, [_P]),
+    ("dem_slab_migrate", C.c_int, [_P, C.c_int, _P, _P, C.c_uint64, C.POINTER(C.c_uint64),
+                                   C.POINTER(C.c_uint64)]),
+    ("dem_slab_import", C.c_int, [_P, _P, C.c_uint64, _P, C.c_uint64]),
+    ("dem_slab_halo", C.c_int, [_P, _P, _P, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    ("dem_slab_ghosts", C.c_int, [_P, _P, C.c_uint64, _P, C.c_uint64]),
+    ("dem_slab_force", C.c_int, [_P, C.c_uint32, C.POINTER(dem_step_metrics)]),
 ]
 
 

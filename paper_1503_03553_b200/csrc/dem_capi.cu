@@ -73,9 +73,29 @@ struct dem_ctx {
     size_t flush_bytes = 0;
     DevCtl* h_ctl = nullptr;  // pinned readback
     dem_error last_error{};
+
+    // slab decomposition (dem_create_slab). Single-GPU contexts: kz0 = 0, nz_loc = nz.
+    bool slab = false;
+    int kz0 = 0, nz_loc = 0;
+    int z_lo = 0, z_hi = 0;
+    uint64_t n_cap = 0;           // slot capacity (owned + ghosts)
+    uint64_t n_own = 0;           // owned slots assembled into Y
+    uint64_t n_asm = 0;           // assembled slots (owned + ghosts)
+    int sstate = 0, shist = 0;    // X = state[sstate], history = hist[shist]
+    bool integrated = false;      // the pending assembly came from an integrating migrate
+    uint32_t* hrm_pos = nullptr;
+    uint32_t* hrm_cnt = nullptr;
+    uint32_t* counters = nullptr;
+    uint32_t* h_counters = nullptr;
+    size_t tile_pairs = 0, imp_cap = 0, imp_used = 0;
+    uint32_t rec_bytes = 0, rec_dt_off = 0, ghost_bytes = 0;
 };
 
 namespace {
+
+int state_cur(const dem_ctx* c) { return c->slab ? c->sstate : static_cast<int>(c->phase_count & 1); }
+int hist_cur(const dem_ctx* c) { return c->slab ? c->shist : static_cast<int>(c->phase_count & 1); }
+uint64_t ft_stride(const dem_ctx* c) { return c->slab ? c->n_cap : c->n; }
 
 int set_error(dem_ctx* c, int code, int kernel, uint32_t slot, uint32_t id, int64_t step, const std::string& msg) {
     if (c) {
@@ -199,10 +219,12 @@ StepParams make_params(const dem_ctx* c, uint32_t flags) {
     p.h = c->grid.cell_size;
     p.inv_h = 1.0 / c->grid.cell_size;  // grid.cpp:32
     p.nx = c->grid.nx; p.ny = c->grid.ny; p.nz = c->grid.nz;
+    p.kz0 = c->kz0;
+    p.nz_loc = c->nz_loc;
     p.M = c->M;
     p.dt = c->dt;
     p.gx = c->gravity[0]; p.gy = c->gravity[1]; p.gz = c->gravity[2];
-    p.n = static_cast<uint32_t>(c->n);
+    p.n = static_cast<uint32_t>(c->slab ? c->n_asm : c->n);
     p.K = c->K;
     p.nmat = static_cast<int>(c->materials.size());
     p.nrect = static_cast<int>(c->rects.size());
@@ -229,7 +251,19 @@ PhaseBufs make_bufs(const dem_ctx* c, uint64_t phase) {
     b.status_scan = c->status_scan; b.status_det = c->status_det;
     b.n_tiles_scan = c->n_tiles_scan; b.n_tiles_det = c->n_tiles_det;
     b.cap = c->cap;
+    b.ft_stride = static_cast<uint32_t>(c->slab ? c->n_cap : c->n);
     b.ctl = c->ctl;
+    if (c->slab) {
+        // slab phase: bin the assembly Y into X; previous history rows reached through the
+        // remapped / imported index (hrm_*), new history into the other history buffer
+        b.src = c->state[c->sstate ^ 1];
+        b.dst = c->state[c->sstate];
+        b.old_h = c->hist[c->shist];
+        b.old_h.pos = c->hrm_pos;
+        b.old_h.cnt = c->hrm_cnt;
+        b.cur_h = c->hist[c->shist ^ 1];
+        b.n_tiles_det = detect_tiles(static_cast<uint32_t>(c->n_asm));
+    }
     return b;
 }
 
@@ -326,15 +360,23 @@ void free_ctx(dem_ctx* c) {
     for (void* p : c->allocations) cudaFree(p);
     if (c->flush_buf) cudaFree(c->flush_buf);
     if (c->h_ctl) cudaFreeHost(c->h_ctl);
+    if (c->h_counters) cudaFreeHost(c->h_counters);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
 
 int allocate(dem_ctx* ctx) {
-    const uint64_t n = ctx->n;
+    const uint64_t n = ctx->slab ? ctx->n_cap : ctx->n;  // slot capacity
     ctx->n_tiles_scan = scan_tiles(ctx->M);
     ctx->n_tiles_det = detect_tiles(static_cast<uint32_t>(n));
-    ctx->cap = static_cast<size_t>(ctx->n_tiles_det) * 32u * static_cast<size_t>(ctx->K);  // tile regions
+    ctx->tile_pairs = static_cast<size_t>(ctx->n_tiles_det) * 32u * static_cast<size_t>(ctx->K);  // tile regions
+    ctx->cap = ctx->tile_pairs + ctx->imp_cap * static_cast<size_t>(ctx->K);  // + history import region
+    if (ctx->slab) {
+        CUDA_TRY(dalloc(ctx, &ctx->hrm_pos, n));
+        CUDA_TRY(dalloc(ctx, &ctx->hrm_cnt, n));
+        CUDA_TRY(dalloc(ctx, &ctx->counters, 8));
+        CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_counters), 8 * sizeof(uint32_t)));
+    }
     for (int b = 0; b < 2; ++b) {
         CUDA_TRY(dalloc(ctx, &ctx->state[b].pos_r, n));
         CUDA_TRY(dalloc(ctx, &ctx->state[b].vel_m, n));
@@ -503,6 +545,8 @@ int dem_create(const dem_config* cfg, const dem_particles* particles, int device
     ctx->collide_variant = cfg->collide_variant;
     ctx->grid = grid;
     ctx->n = particles->count;
+    ctx->kz0 = 0;
+    ctx->nz_loc = grid.nz;
     ctx->M = static_cast<uint32_t>(static_cast<int64_t>(grid.nx) * grid.ny * grid.nz);
     rc = allocate(ctx);
     if (rc == DEM_OK) rc = upload_tables(ctx);
@@ -527,7 +571,7 @@ int dem_create(const dem_config* cfg, const dem_particles* particles, int device
 }
 
 int dem_clone(const dem_ctx* src, dem_ctx** out) {
-    if (!src || !out) return DEM_ERR_ARGUMENT;
+    if (!src || !out || src->slab) return DEM_ERR_ARGUMENT;
     dem_ctx* ctx = new (std::nothrow) dem_ctx();
     if (!ctx) return DEM_ERR_ARGUMENT;
     ctx->device = src->device;
@@ -543,6 +587,7 @@ int dem_clone(const dem_ctx* src, dem_ctx** out) {
     ctx->rects = src->rects; ctx->lines = src->lines;
     ctx->grid_cell_size = src->grid_cell_size; ctx->K = src->K; ctx->collide_variant = src->collide_variant;
     ctx->grid = src->grid; ctx->n = src->n; ctx->M = src->M;
+    ctx->kz0 = src->kz0; ctx->nz_loc = src->nz_loc;
     int rc = allocate(ctx);
     if (rc == DEM_OK) {
         // allocations were made in the same order with the same sizes: copy pairwise
@@ -623,7 +668,7 @@ int dem_get_particles(dem_ctx* ctx, dem_particles* out) {
     if (!ctx || !out || out->count != ctx->n) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
     const uint64_t n = ctx->n;
-    const StateBuf& s = ctx->state[ctx->phase_count & 1];
+    const StateBuf& s = ctx->state[state_cur(ctx)];
     std::vector<double4> pr(n), vm(n), om(n);
     std::vector<uint2> idm(n);
     if (n) {
@@ -650,22 +695,22 @@ int dem_set_particles(dem_ctx* ctx, const dem_particles* in) {
     if (!in->ids || !in->positions || !in->velocities || !in->angular_velocities || !in->radii || !in->masses || !in->material_ids)
         return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
-    return upload_state(ctx, in, static_cast<int>(ctx->phase_count & 1));
+    return upload_state(ctx, in, state_cur(ctx));
 }
 
 int dem_get_forces(dem_ctx* ctx, double* force, double* torque) {
     if (!ctx) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
-    const uint64_t n = ctx->n;
-    std::vector<double> ft(6 * n);
+    const uint64_t n = ctx->n, fs = ft_stride(ctx);
+    std::vector<double> ft(6 * fs);
     if (n) {
-        CUDA_TRY(cudaMemcpyAsync(ft.data(), ctx->ft, 6 * n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(ft.data(), ctx->ft, 6 * fs * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
         CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     }
     for (uint64_t i = 0; i < n; ++i)
         for (int a = 0; a < 3; ++a) {
-            if (force) force[3 * i + a] = ft[a * n + i];
-            if (torque) torque[3 * i + a] = ft[(3 + a) * n + i];
+            if (force) force[3 * i + a] = ft[a * fs + i];
+            if (torque) torque[3 * i + a] = ft[(3 + a) * fs + i];
         }
     return DEM_OK;
 }
@@ -673,12 +718,12 @@ int dem_get_forces(dem_ctx* ctx, double* force, double* torque) {
 int dem_set_forces(dem_ctx* ctx, const double* force, const double* torque) {
     if (!ctx || !force || !torque) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
-    const uint64_t n = ctx->n;
-    std::vector<double> ft(6 * n);
+    const uint64_t n = ctx->n, fs = ft_stride(ctx);
+    std::vector<double> ft(6 * fs, 0.0);
     for (uint64_t i = 0; i < n; ++i)
-        for (int a = 0; a < 3; ++a) { ft[a * n + i] = force[3 * i + a]; ft[(3 + a) * n + i] = torque[3 * i + a]; }
+        for (int a = 0; a < 3; ++a) { ft[a * fs + i] = force[3 * i + a]; ft[(3 + a) * fs + i] = torque[3 * i + a]; }
     if (n) {
-        CUDA_TRY(cudaMemcpyAsync(ctx->ft, ft.data(), 6 * n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_TRY(cudaMemcpyAsync(ctx->ft, ft.data(), 6 * fs * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
         CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     }
     return DEM_OK;
@@ -705,7 +750,7 @@ int64_t dem_get_contacts(dem_ctx* ctx, uint32_t* owner_slot, int32_t* partner, d
     cudaSetDevice(ctx->device);
     const uint64_t n = ctx->n;
     if (n == 0) return 0;
-    const HistBuf& h = ctx->hist[ctx->phase_count & 1];
+    const HistBuf& h = ctx->hist[hist_cur(ctx)];
     std::vector<uint32_t> pos(n), cnt(n);
     if (cudaMemcpy(pos.data(), h.pos, n * sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess) return -DEM_ERR_CUDA;
     if (cudaMemcpy(cnt.data(), h.cnt, n * sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess) return -DEM_ERR_CUDA;
@@ -785,6 +830,219 @@ int dem_profile_step(dem_ctx* ctx, size_t flush_bytes, dem_step_metrics* m) {
     }
     for (auto& e : ev) cudaEventDestroy(e);
     return rc;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Slab decomposition. The host moves records between neighbours
+// (NCCL over NVLink in production, gloo / loopback in tests); these calls only touch device
+// memory they are given.
+
+namespace {
+
+SlabBufs make_slab(const dem_ctx* c, void* send_lo, void* send_hi, uint64_t cap_records) {
+    SlabBufs s{};
+    s.X = c->state[c->sstate];
+    s.Y = c->state[c->sstate ^ 1];
+    s.ft = c->ft;
+    s.ft_stride = static_cast<uint32_t>(c->n_cap);
+    s.H_old = c->hist[c->shist];
+    s.hrm_pos = c->hrm_pos;
+    s.hrm_cnt = c->hrm_cnt;
+    s.n_x = static_cast<uint32_t>(c->n);
+    s.counters = c->counters;
+    s.send_lo = static_cast<uint8_t*>(send_lo);
+    s.send_hi = static_cast<uint8_t*>(send_hi);
+    s.cap_send = static_cast<uint32_t>(std::min<uint64_t>(cap_records, 0xffffffffull));
+    s.rec_bytes = c->rec_bytes;
+    s.rec_dt_off = c->rec_dt_off;
+    s.ghost_bytes = c->ghost_bytes;
+    s.z_lo = c->z_lo;
+    s.z_hi = c->z_hi;
+    s.imp_base = c->tile_pairs;
+    s.hcap = c->cap;
+    s.K = static_cast<uint32_t>(c->K);
+    s.ctl = c->ctl;
+    return s;
+}
+
+int read_counters(dem_ctx* ctx) {
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_counters, ctx->counters, 8 * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    CUDA_TRY(cudaGetLastError());
+    return DEM_OK;
+}
+
+}  // namespace
+
+int dem_create_slab(const dem_config* cfg, const dem_particles* owned, int device, int32_t z_lo, int32_t z_hi,
+                    uint64_t capacity, dem_ctx** out) {
+    if (!cfg || !owned || !out) return DEM_ERR_ARGUMENT;
+    *out = nullptr;
+    std::string why;
+    int rc = validate(cfg, owned, &why);
+    if (rc == DEM_OK && !(cfg->grid_cell_size > 0.0)) {
+        why = "grid.cell_size: a slab context needs the global cell size (2 r_max (1 + 1e-6) of all ranks)";
+        rc = DEM_ERR_CONFIG;
+    }
+    dem_grid grid{};
+    if (rc == DEM_OK) rc = make_grid(cfg, 0.0, &grid, &why);
+    if (rc == DEM_OK && !(z_lo >= 0 && z_lo < z_hi && z_hi <= grid.nz)) {
+        why = "slab planes must satisfy 0 <= z_lo < z_hi <= nz";
+        rc = DEM_ERR_CONFIG;
+    }
+    if (rc != DEM_OK) {
+        std::snprintf(g_create_error.message, sizeof(g_create_error.message), "%s", why.c_str());
+        g_create_error.code = rc;
+        return rc;
+    }
+    dem_ctx* ctx = new (std::nothrow) dem_ctx();
+    if (!ctx) return DEM_ERR_ARGUMENT;
+    ctx->device = device;
+    if (cudaSetDevice(device) != cudaSuccess || cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        free_ctx(ctx);
+        return DEM_ERR_CUDA;
+    }
+    cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+    init_device_attributes();
+    ctx->dt = cfg->dt;
+    for (int a = 0; a < 3; ++a) {
+        ctx->gravity[a] = cfg->gravity[a];
+        ctx->domain_min[a] = cfg->domain_min[a];
+        ctx->domain_max[a] = cfg->domain_max[a];
+    }
+    ctx->materials.assign(cfg->materials, cfg->materials + cfg->material_count);
+    if (cfg->pair_restitution)
+        ctx->pair_rest.assign(cfg->pair_restitution, cfg->pair_restitution + cfg->material_count * cfg->material_count);
+    if (cfg->rect_wall_count) ctx->rects.assign(cfg->rect_walls, cfg->rect_walls + cfg->rect_wall_count);
+    if (cfg->line_wall_count) ctx->lines.assign(cfg->line_walls, cfg->line_walls + cfg->line_wall_count);
+    ctx->grid_cell_size = cfg->grid_cell_size;
+    ctx->K = cfg->contact_capacity;
+    ctx->collide_variant = cfg->collide_variant;
+    ctx->grid = grid;
+    ctx->slab = true;
+    ctx->z_lo = z_lo;
+    ctx->z_hi = z_hi;
+    ctx->kz0 = std::max(z_lo - 1, 0);
+    ctx->nz_loc = std::min(z_hi + 1, grid.nz) - ctx->kz0;
+    ctx->M = static_cast<uint32_t>(static_cast<int64_t>(grid.nx) * grid.ny * ctx->nz_loc);
+    ctx->n = owned->count;
+    ctx->n_cap = std::max<uint64_t>(capacity, owned->count) + 32;
+    ctx->imp_cap = ctx->n_cap / 4 + 1024;
+    const uint32_t keys_bytes = ((4u * ctx->K) + 7u) & ~7u;
+    ctx->rec_dt_off = 112u + keys_bytes;
+    ctx->rec_bytes = (ctx->rec_dt_off + 24u * ctx->K + 31u) & ~31u;
+    ctx->ghost_bytes = 128u;
+    ctx->sstate = 0;
+    ctx->shist = 0;
+    rc = allocate(ctx);
+    if (rc == DEM_OK) rc = upload_tables(ctx);
+    if (rc == DEM_OK) {
+        DevCtl init{};
+        init.err_key = kNoError;
+        for (auto& s : init.err_sid) s = kNoError;
+        if (cudaMemcpy(ctx->ctl, &init, sizeof(DevCtl), cudaMemcpyHostToDevice) != cudaSuccess) rc = DEM_ERR_CUDA;
+    }
+    if (rc == DEM_OK) rc = upload_state(ctx, owned, 0);
+    if (rc != DEM_OK) {
+        g_create_error = ctx->last_error;
+        g_create_error.code = rc;
+        free_ctx(ctx);
+        return rc;
+    }
+    *out = ctx;
+    return DEM_OK;
+}
+
+int dem_slab_record_bytes(const dem_ctx* ctx, uint64_t* migrant_bytes, uint64_t* ghost_bytes) {
+    if (!ctx || !ctx->slab) return DEM_ERR_ARGUMENT;
+    if (migrant_bytes) *migrant_bytes = ctx->rec_bytes;
+    if (ghost_bytes) *ghost_bytes = ctx->ghost_bytes;
+    return DEM_OK;
+}
+
+uint64_t dem_slab_owned(const dem_ctx* ctx) { return ctx && ctx->slab ? ctx->n_own : 0; }
+
+int dem_slab_migrate(dem_ctx* ctx, int integrate, void* send_lo, void* send_hi, uint64_t cap_records,
+                     uint64_t* n_lo, uint64_t* n_hi) {
+    if (!ctx || !ctx->slab || !n_lo || !n_hi) return DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    CUDA_TRY(cudaMemsetAsync(ctx->counters, 0, 8 * sizeof(uint32_t), ctx->stream));
+    const StepParams p = make_params(ctx, 0);
+    launch_slab_migrate(p, make_slab(ctx, send_lo, send_hi, cap_records), integrate != 0, ctx->stream);
+    int rc = read_counters(ctx);
+    if (rc == DEM_OK) rc = collect(ctx, nullptr, ctx->phase_count, ctx->step_index, false);
+    if (rc != DEM_OK) return rc;
+    if (ctx->h_counters[4]) return set_error(ctx, DEM_ERR_CAPACITY, -1, 0, 0, ctx->step_index, "slab: migrant send buffer too small");
+    ctx->n_own = ctx->h_counters[0];
+    ctx->n_asm = ctx->n_own;
+    ctx->imp_used = 0;
+    ctx->integrated = integrate != 0;
+    *n_lo = ctx->h_counters[1];
+    *n_hi = ctx->h_counters[2];
+    return DEM_OK;
+}
+
+int dem_slab_import(dem_ctx* ctx, const void* recs_lo, uint64_t n_lo, const void* recs_hi, uint64_t n_hi) {
+    if (!ctx || !ctx->slab) return DEM_ERR_ARGUMENT;
+    if (ctx->n_own + n_lo + n_hi > ctx->n_cap || (ctx->imp_used / ctx->K) + n_lo + n_hi > ctx->imp_cap)
+        return set_error(ctx, DEM_ERR_CAPACITY, -1, 0, 0, ctx->step_index, "slab: context capacity exceeded by imports");
+    cudaSetDevice(ctx->device);
+    const SlabBufs s = make_slab(ctx, nullptr, nullptr, 0);
+    launch_slab_import(s, recs_lo, static_cast<uint32_t>(n_lo), static_cast<uint32_t>(ctx->n_own), ctx->imp_used, ctx->stream);
+    ctx->n_own += n_lo;
+    ctx->imp_used += n_lo * ctx->K;
+    launch_slab_import(s, recs_hi, static_cast<uint32_t>(n_hi), static_cast<uint32_t>(ctx->n_own), ctx->imp_used, ctx->stream);
+    ctx->n_own += n_hi;
+    ctx->imp_used += n_hi * ctx->K;
+    ctx->n_asm = ctx->n_own;
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    CUDA_TRY(cudaGetLastError());
+    return DEM_OK;
+}
+
+int dem_slab_halo(dem_ctx* ctx, void* send_lo, void* send_hi, uint64_t cap_records, uint64_t* n_lo, uint64_t* n_hi) {
+    if (!ctx || !ctx->slab || !n_lo || !n_hi) return DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    CUDA_TRY(cudaMemsetAsync(ctx->counters, 0, 8 * sizeof(uint32_t), ctx->stream));
+    const StepParams p = make_params(ctx, 0);
+    launch_slab_halo(p, make_slab(ctx, send_lo, send_hi, cap_records), static_cast<uint32_t>(ctx->n_own), ctx->stream);
+    int rc = read_counters(ctx);
+    if (rc != DEM_OK) return rc;
+    if (ctx->h_counters[4]) return set_error(ctx, DEM_ERR_CAPACITY, -1, 0, 0, ctx->step_index, "slab: halo send buffer too small");
+    *n_lo = ctx->h_counters[5];
+    *n_hi = ctx->h_counters[6];
+    return DEM_OK;
+}
+
+int dem_slab_ghosts(dem_ctx* ctx, const void* recs_lo, uint64_t n_lo, const void* recs_hi, uint64_t n_hi) {
+    if (!ctx || !ctx->slab) return DEM_ERR_ARGUMENT;
+    if (ctx->n_own + n_lo + n_hi > ctx->n_cap)
+        return set_error(ctx, DEM_ERR_CAPACITY, -1, 0, 0, ctx->step_index, "slab: context capacity exceeded by ghosts");
+    cudaSetDevice(ctx->device);
+    const SlabBufs s = make_slab(ctx, nullptr, nullptr, 0);
+    launch_slab_ghosts(s, recs_lo, static_cast<uint32_t>(n_lo), static_cast<uint32_t>(ctx->n_own), ctx->stream);
+    launch_slab_ghosts(s, recs_hi, static_cast<uint32_t>(n_hi), static_cast<uint32_t>(ctx->n_own + n_lo), ctx->stream);
+    ctx->n_asm = ctx->n_own + n_lo + n_hi;
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    CUDA_TRY(cudaGetLastError());
+    return DEM_OK;
+}
+
+int dem_slab_force(dem_ctx* ctx, uint32_t flags, dem_step_metrics* m) {
+    if (!ctx || !ctx->slab) return DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    flags = (flags & ~static_cast<uint32_t>(DEM_PHASE_INTEGRATE)) | kPhaseSlab;
+    const uint64_t pb = ctx->phase_count;
+    const int64_t sb = ctx->step_index;
+    ++ctx->phase_count;
+    if (ctx->integrated) ++ctx->step_index;
+    enqueue_phase(ctx, flags, ctx->phase_count, nullptr);
+    const int rc = collect(ctx, m, pb, sb, ctx->integrated);
+    ctx->integrated = false;
+    if (rc != DEM_OK) return rc;
+    ctx->n = ctx->n_asm;
+    ctx->shist ^= 1;
+    return DEM_OK;
 }
 
 }  // extern "C"

@@ -13,6 +13,7 @@ constexpr int kMaxMaterials = 16;
 constexpr int kMaxWalls = 64;
 constexpr uint32_t kWallBit = 0x80000000u;  // partner codes >= this are walls: ~code = wall index
 constexpr unsigned long long kNoError = ~0ull;
+constexpr uint32_t kPhaseSlab = 64u;  // internal phase flag: slab context (ghost-aware kernels)
 
 struct MatPairH {  // host mirror of MatPair (dem_math.cuh)
     double shear_sum, young_sum, alpha, mu;
@@ -30,8 +31,9 @@ struct LineW {
 struct StepParams {
     double ox, oy, oz;   // grid origin
     double h, inv_h;     // cell size, 1.0 / h (grid.cpp:32)
-    int nx, ny, nz;
-    uint32_t M;          // nx*ny*nz
+    int nx, ny, nz;      // GLOBAL grid (grid.cpp:10-28)
+    int kz0, nz_loc;     // keyed z-planes [kz0, kz0+nz_loc) (slab context; else 0, nz)
+    uint32_t M;          // keyed cells nx*ny*nz_loc
     double dt;
     double gx, gy, gz;
     uint32_t n;          // particles
@@ -96,9 +98,37 @@ struct PhaseBufs {
     unsigned long long* status_scan;
     unsigned long long* status_det;
     uint32_t n_tiles_scan, n_tiles_det;
-    size_t cap;              // pair capacity
+    size_t cap;              // pair slots in key/dt (SoA stride of dt)
+    uint32_t ft_stride;      // SoA stride of ft (n, or the slab context's slot capacity)
     DevCtl* ctl;
 };
+
+// Slab decomposition buffers (dem_slab.cu). X: state after the previous force phase (owned and
+// ghosts); Y: the assembly buffer the next force phase bins from.
+struct SlabBufs {
+    StateBuf X, Y;
+    const double* ft;
+    uint32_t ft_stride;
+    HistBuf H_old;           // previous phase's history (pos/cnt per X slot), + import region
+    uint32_t* hrm_pos;       // per Y slot: previous history row (remapped / imported)
+    uint32_t* hrm_cnt;
+    uint32_t n_x;
+    uint32_t* counters;      // [0] stayers [1] to lo [2] to hi [4] overflow [5] halo lo [6] halo hi
+    uint8_t* send_lo;
+    uint8_t* send_hi;
+    uint32_t cap_send;       // records per send buffer
+    uint32_t rec_bytes, rec_dt_off, ghost_bytes;
+    int z_lo, z_hi;          // owned global planes
+    size_t imp_base;         // first pair slot of the history import region
+    size_t hcap;             // pair slots in key/dt (SoA stride)
+    uint32_t K;
+    DevCtl* ctl;
+};
+
+void launch_slab_migrate(const StepParams& p, const SlabBufs& s, bool integrate, cudaStream_t st);
+void launch_slab_import(const SlabBufs& s, const void* recs, uint32_t n, uint32_t base, size_t imp_off, cudaStream_t st);
+void launch_slab_halo(const StepParams& p, const SlabBufs& s, uint32_t n_own, cudaStream_t st);
+void launch_slab_ghosts(const SlabBufs& s, const void* recs, uint32_t n, uint32_t base, cudaStream_t st);
 
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;

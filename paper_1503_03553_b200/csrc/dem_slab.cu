@@ -1,0 +1,193 @@
+// dem_slab.cu — slab domain decomposition kernels.
+//
+// A slab context owns the particles whose GLOBAL cell z lies in [z_lo, z_hi) and holds, for
+// each step, a one-plane halo of neighbour particles (ghosts) below and above. Per step:
+//   k_slab_migrate  integrate the owned particles (pipeline.cpp:31-44), classify them by their
+//                   new cell plane, compact the stayers into the assembly buffer Y (carrying the
+//                   index of their previous history row) and write leavers, with their history
+//                   rows keyed by stable id, as migrant records for the neighbour;
+//   k_slab_import   append received migrants to Y and their history rows to the import region;
+//   k_slab_halo     write boundary-plane owned particles as ghost records for the neighbours;
+//   k_slab_ghosts   append received ghosts to Y, flagged (idm.y bit 31).
+// The force phase then bins Y (owned + ghosts) into X and detects / computes forces for owned
+// slots only. Because the in-cell order is canonical (cell, stable id), every owned particle
+// sees exactly the candidate sequence of a single-GPU run: results are bitwise identical to
+// one GPU. The order in which records are written here (atomics) does not matter for that.
+#include <cuda_runtime.h>
+
+#include "dem_internal.h"
+#include "dem_math.cuh"
+
+namespace demb200 {
+
+namespace {
+
+constexpr uint32_t kGhost = 0x80000000u;
+
+__device__ __forceinline__ void raise_err(DevCtl* ctl, int kernel, uint32_t slot, uint32_t id, int code) {
+    const unsigned long long key = (static_cast<unsigned long long>(kernel) << 56) |
+                                   (static_cast<unsigned long long>(slot) << 8) | static_cast<unsigned long long>(code);
+    atomicMin(&ctl->err_key, key);
+    atomicMin(&ctl->err_sid[kernel], (static_cast<unsigned long long>(slot) << 32) | id);
+    ctl->err_phase = ctl->phase;
+}
+
+// global cell plane of a position: the z part of calc_hash (grid.cpp:30-52)
+__device__ __forceinline__ int cell_z(const StepParams& p, double z) {
+    int cz = to_int_x86(floor((z - p.oz) * p.inv_h));
+    return cz < 0 ? 0 : (cz >= p.nz ? p.nz - 1 : cz);
+}
+
+// warp-aggregated counter increment among lanes with the same `cls`
+__device__ __forceinline__ uint32_t agg_add(uint32_t* ctr, int cls) {
+    const unsigned active = __activemask();
+    const unsigned peers = __match_any_sync(active, cls);
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(ctr, static_cast<uint32_t>(__popc(peers)));
+    base = __shfl_sync(peers, base, leader);
+    return base + __popc(peers & ((1u << lane) - 1u));
+}
+
+__device__ __forceinline__ void put_state(StateBuf& y, uint32_t s, double4 pr, double4 vm, double4 om, uint2 idm) {
+    st4(&y.pos_r[s], pr);
+    st4(&y.vel_m[s], vm);
+    st4(&y.omg[s], om);
+    y.idm[s] = idm;
+}
+
+__device__ __forceinline__ void put_record(uint8_t* rec, double4 pr, double4 vm, double4 om, uint2 idm) {
+    double4* d = reinterpret_cast<double4*>(rec);
+    st4(&d[0], pr);
+    st4(&d[1], vm);
+    st4(&d[2], om);
+    *reinterpret_cast<uint2*>(rec + 96) = idm;
+}
+
+template <bool INTEGRATE>
+__global__ void __launch_bounds__(256) k_slab_migrate(StepParams p, SlabBufs s) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= s.n_x) return;
+    const uint2 idm = s.X.idm[i];
+    if (idm.y & kGhost) return;  // last step's halo copies are dropped
+    double4 pr = ld4(&s.X.pos_r[i]);
+    double4 vm = ld4(&s.X.vel_m[i]);
+    double4 om = ld4(&s.X.omg[i]);
+    if (INTEGRATE) {  // pipeline.cpp:31-44, same arithmetic as k_integrate_hash
+        const uint32_t n = s.ft_stride;
+        const V3 f = v3(s.ft[i], s.ft[n + i], s.ft[2 * n + i]);
+        const V3 t = v3(s.ft[3 * n + i], s.ft[4 * n + i], s.ft[5 * n + i]);
+        if (!finite3(f) || !finite3(t)) {
+            raise_err(s.ctl, 0, i, idm.x, 2 /*DEM_ERR_KERNEL*/);
+        } else {
+            const double m = vm.w, r = pr.w;
+            const double sc = p.dt / m;
+            vm.x = vm.x + f.x * sc; vm.y = vm.y + f.y * sc; vm.z = vm.z + f.z * sc;
+            pr.x = pr.x + vm.x * p.dt; pr.y = pr.y + vm.y * p.dt; pr.z = pr.z + vm.z * p.dt;
+            const double inertia = 0.4 * m * r * r;
+            const double s2 = p.dt / inertia;
+            om.x = om.x + t.x * s2; om.y = om.y + t.y * s2; om.z = om.z + t.z * s2;
+        }
+    }
+    const int cz = cell_z(p, pr.z);
+    const int cls = cz < s.z_lo ? 1 : (cz >= s.z_hi ? 2 : 0);
+    const uint32_t slot = agg_add(&s.counters[cls], cls);
+    const uint32_t hpos = s.H_old.pos[i], hcnt = s.H_old.cnt[i];
+    if (cls == 0) {
+        put_state(s.Y, slot, pr, vm, om, idm);
+        s.hrm_pos[slot] = hpos;
+        s.hrm_cnt[slot] = hcnt;
+        return;
+    }
+    if (slot >= s.cap_send) { atomicMax(&s.counters[4], 1u); return; }
+    uint8_t* rec = (cls == 1 ? s.send_lo : s.send_hi) + static_cast<size_t>(slot) * s.rec_bytes;
+    put_record(rec, pr, vm, om, idm);
+    uint32_t* hdr = reinterpret_cast<uint32_t*>(rec + 104);
+    hdr[0] = hcnt;
+    uint32_t* keys = reinterpret_cast<uint32_t*>(rec + 112);
+    double* dts = reinterpret_cast<double*>(rec + s.rec_dt_off);
+    for (uint32_t k = 0; k < hcnt; ++k) {
+        keys[k] = s.H_old.key[hpos + k];
+        dts[3 * k + 0] = s.H_old.dt[hpos + k];
+        dts[3 * k + 1] = s.H_old.dt[s.hcap + hpos + k];
+        dts[3 * k + 2] = s.H_old.dt[2 * s.hcap + hpos + k];
+    }
+}
+
+__global__ void __launch_bounds__(256) k_slab_import(SlabBufs s, const uint8_t* recs, uint32_t n, uint32_t base,
+                                                      size_t imp_off) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint8_t* rec = recs + static_cast<size_t>(t) * s.rec_bytes;
+    const double4* d = reinterpret_cast<const double4*>(rec);
+    const uint2 idm = *reinterpret_cast<const uint2*>(rec + 96);
+    put_state(s.Y, base + t, ld4(&d[0]), ld4(&d[1]), ld4(&d[2]), idm);
+    const uint32_t hcnt = reinterpret_cast<const uint32_t*>(rec + 104)[0];
+    const uint32_t* keys = reinterpret_cast<const uint32_t*>(rec + 112);
+    const double* dts = reinterpret_cast<const double*>(rec + s.rec_dt_off);
+    const size_t hpos = s.imp_base + imp_off + static_cast<size_t>(t) * s.K;
+    for (uint32_t k = 0; k < hcnt; ++k) {
+        s.H_old.key[hpos + k] = keys[k];
+        s.H_old.dt[hpos + k] = dts[3 * k];
+        s.H_old.dt[s.hcap + hpos + k] = dts[3 * k + 1];
+        s.H_old.dt[2 * s.hcap + hpos + k] = dts[3 * k + 2];
+    }
+    s.hrm_pos[base + t] = static_cast<uint32_t>(hpos);
+    s.hrm_cnt[base + t] = hcnt;
+}
+
+// owned particles of Y[0, n_own) on the boundary planes become ghost records for the neighbours
+__global__ void __launch_bounds__(256) k_slab_halo(StepParams p, SlabBufs s, uint32_t n_own) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_own) return;
+    const double4 pr = ld4(&s.Y.pos_r[i]);
+    const int cz = cell_z(p, pr.z);
+    const bool lo = cz == s.z_lo, hi = cz == s.z_hi - 1;
+    if (!lo && !hi) return;
+    const double4 vm = ld4(&s.Y.vel_m[i]), om = ld4(&s.Y.omg[i]);
+    const uint2 idm = s.Y.idm[i];
+    if (lo) {
+        const uint32_t slot = atomicAdd(&s.counters[5], 1u);
+        if (slot < s.cap_send) put_record(s.send_lo + static_cast<size_t>(slot) * s.ghost_bytes, pr, vm, om, idm);
+        else atomicMax(&s.counters[4], 1u);
+    }
+    if (hi) {
+        const uint32_t slot = atomicAdd(&s.counters[6], 1u);
+        if (slot < s.cap_send) put_record(s.send_hi + static_cast<size_t>(slot) * s.ghost_bytes, pr, vm, om, idm);
+        else atomicMax(&s.counters[4], 1u);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_slab_ghosts(SlabBufs s, const uint8_t* recs, uint32_t n, uint32_t base) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint8_t* rec = recs + static_cast<size_t>(t) * s.ghost_bytes;
+    const double4* d = reinterpret_cast<const double4*>(rec);
+    uint2 idm = *reinterpret_cast<const uint2*>(rec + 96);
+    idm.y |= kGhost;
+    put_state(s.Y, base + t, ld4(&d[0]), ld4(&d[1]), ld4(&d[2]), idm);
+    s.hrm_pos[base + t] = 0;
+    s.hrm_cnt[base + t] = 0;
+}
+
+inline unsigned blocks(size_t n) { return static_cast<unsigned>((n + 255) / 256); }
+
+}  // namespace
+
+void launch_slab_migrate(const StepParams& p, const SlabBufs& s, bool integrate, cudaStream_t st) {
+    if (!s.n_x) return;
+    if (integrate) k_slab_migrate<true><<<blocks(s.n_x), 256, 0, st>>>(p, s);
+    else k_slab_migrate<false><<<blocks(s.n_x), 256, 0, st>>>(p, s);
+}
+void launch_slab_import(const SlabBufs& s, const void* recs, uint32_t n, uint32_t base, size_t imp_off, cudaStream_t st) {
+    if (n) k_slab_import<<<blocks(n), 256, 0, st>>>(s, static_cast<const uint8_t*>(recs), n, base, imp_off);
+}
+void launch_slab_halo(const StepParams& p, const SlabBufs& s, uint32_t n_own, cudaStream_t st) {
+    if (n_own) k_slab_halo<<<blocks(n_own), 256, 0, st>>>(p, s, n_own);
+}
+void launch_slab_ghosts(const SlabBufs& s, const void* recs, uint32_t n, uint32_t base, cudaStream_t st) {
+    if (n) k_slab_ghosts<<<blocks(n), 256, 0, st>>>(s, static_cast<const uint8_t*>(recs), n, base);
+}
+
+}  // namespace demb200

@@ -1,0 +1,319 @@
+"""Slab domain decomposition of the DEM step over several GPUs.
+
+The reference is single-process; this is the B200 build's multi-GPU path. Space is
+cut into slabs of whole cell planes along z, balanced by particle count. Each rank owns the
+particles whose cell plane lies in its slab, and each step it:
+
+  1. integrates its owned particles and hands the ones whose plane left the slab, with their
+     tangential-history rows (keyed by stable id), to the z-neighbour          (migrate/import)
+  2. sends its boundary-plane particles to the neighbours as ghosts             (halo/ghosts)
+  3. bins owned + ghosts, detects and computes forces for owned particles only  (force)
+
+Exchanges are neighbour point-to-point transfers: NCCL over NVLink when the transport is
+torch.distributed with backend "nccl" (device tensors), gloo in CPU tests, or an in-process
+loopback (several ranks on one GPU, for single-GPU validation). The canonical in-cell order
+(cell, stable id) makes the result bitwise identical to a single-GPU run for any rank count.
+
+This module holds the protocol (partitioning, the exchange pattern, the phase order) and the
+CUDA-backed rank. The test suite drives the same protocol with a CPU oracle-backed rank
+(tests/slab_oracle_backend.py) over gloo.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, replace
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _capi
+from .simulation import ParticleSet, SimConfig, StepMetrics, _Config, _raise
+
+GHOST_BIT = 0x80000000
+
+
+# ---------------------------------------------------------------------------------------------
+# Partitioning (pure host arithmetic, identical on every rank)
+
+@dataclass
+class GlobalGrid:
+    oz: float
+    h: float
+    inv_h: float
+    nz: int
+
+
+def global_grid(cfg: SimConfig, r_max: float) -> GlobalGrid:
+    """make_grid (grid.cpp:10-28) for the z axis, with the cell size every rank must share."""
+    h = cfg.grid_cell_size if cfg.grid_cell_size > 0.0 else 2.0 * r_max * (1.0 + 1e-6)
+    ez = cfg.domain_max[2] - cfg.domain_min[2]
+    nz = max(1, int(math.ceil(ez / h)))
+    return GlobalGrid(cfg.domain_min[2], h, 1.0 / h, nz)
+
+
+def cell_planes(z: np.ndarray, g: GlobalGrid) -> np.ndarray:
+    """z part of calc_hash (grid.cpp:30-52): floor((z - origin) * (1/h)), clamped."""
+    f = np.floor((np.asarray(z, np.float64) - g.oz) * g.inv_h)
+    f = np.where(np.isfinite(f), f, -1.0)
+    return np.clip(f, 0, g.nz - 1).astype(np.int64)
+
+
+def slab_bounds(planes: np.ndarray, nz: int, nranks: int) -> List[tuple]:
+    """Contiguous plane ranges [z_lo, z_hi) with balanced particle counts, >= 1 plane each."""
+    if nranks > nz:
+        raise ValueError(f"{nranks} slabs need at least {nranks} cell planes (grid has {nz})")
+    hist = np.bincount(planes, minlength=nz).astype(np.float64)
+    cum = np.cumsum(hist)
+    total = cum[-1] if len(cum) else 0.0
+    cuts = [0]
+    for k in range(1, nranks):
+        target = total * k / nranks
+        z = int(np.searchsorted(cum, target, side="left")) + 1
+        z = max(z, cuts[-1] + 1)
+        z = min(z, nz - (nranks - k))
+        cuts.append(z)
+    cuts.append(nz)
+    return [(cuts[k], cuts[k + 1]) for k in range(nranks)]
+
+
+def select(ps: ParticleSet, mask: np.ndarray) -> ParticleSet:
+    out = ParticleSet(0)
+    for k in ("ids", "positions", "velocities", "angular_velocities", "radii", "masses", "material_ids"):
+        setattr(out, k, np.ascontiguousarray(getattr(ps, k)[mask]))
+    return out
+
+
+# ---------------------------------------------------------------------------------------------
+# Transports
+
+class LoopbackTransport:
+    """Several ranks in one process (e.g. on one GPU): records are copied between the ranks'
+    buffers directly. Used to validate the decomposition on a single device."""
+
+    def __init__(self, ranks):
+        self.ranks = ranks
+
+    def exchange(self, kind: str):
+        R = len(self.ranks)
+        for r, rk in enumerate(self.ranks):
+            rk.recv_count[kind] = [0, 0]
+        for r, rk in enumerate(self.ranks):
+            n_lo, n_hi = rk.send_count[kind]
+            if r > 0 and n_lo:  # to r-1, which receives it from above
+                self.ranks[r - 1].receive(kind, 1, rk.send_view(kind, 0, n_lo), n_lo)
+            if r < R - 1 and n_hi:
+                self.ranks[r + 1].receive(kind, 0, rk.send_view(kind, 1, n_hi), n_hi)
+
+
+class TorchTransport:
+    """One rank per process over torch.distributed: counts, then payloads, to the z-neighbours
+    with batched isend/irecv (NCCL P2P over NVLink for device buffers; gloo for CPU buffers)."""
+
+    def __init__(self, rank: int, world: int):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.rank, self.world = rank, world
+        self.ranks = None
+
+    def bind(self, rk):
+        self.ranks = [rk]
+
+    def exchange(self, kind: str):
+        torch, dist = self.torch, self.dist
+        rk = self.ranks[0]
+        dev = rk.buffer_device()
+        n_lo, n_hi = rk.send_count[kind]
+        lo, hi = self.rank - 1, self.rank + 1
+        c_send = [torch.tensor([n_lo], dtype=torch.int64, device=dev), torch.tensor([n_hi], dtype=torch.int64, device=dev)]
+        c_recv = [torch.zeros(1, dtype=torch.int64, device=dev), torch.zeros(1, dtype=torch.int64, device=dev)]
+        ops = []
+        if lo >= 0:
+            ops += [dist.P2POp(dist.isend, c_send[0], lo), dist.P2POp(dist.irecv, c_recv[0], lo)]
+        if hi < self.world:
+            ops += [dist.P2POp(dist.isend, c_send[1], hi), dist.P2POp(dist.irecv, c_recv[1], hi)]
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        m_lo, m_hi = int(c_recv[0].item()), int(c_recv[1].item())
+        rk.recv_count[kind] = [0, 0]
+        ops = []
+        if lo >= 0 and n_lo:
+            ops.append(dist.P2POp(dist.isend, rk.send_view(kind, 0, n_lo), lo))
+        if lo >= 0 and m_lo:
+            ops.append(dist.P2POp(dist.irecv, rk.recv_view(kind, 0, m_lo), lo))
+        if hi < self.world and n_hi:
+            ops.append(dist.P2POp(dist.isend, rk.send_view(kind, 1, n_hi), hi))
+        if hi < self.world and m_hi:
+            ops.append(dist.P2POp(dist.irecv, rk.recv_view(kind, 1, m_hi), hi))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        if dev.type == "cuda":
+            torch.cuda.current_stream(dev).synchronize()
+        rk.recv_count[kind] = [m_lo, m_hi]
+
+
+# ---------------------------------------------------------------------------------------------
+# The CUDA-backed rank
+
+class SlabRankCuda:
+    """One slab on one GPU: a dem_create_slab context plus its record buffers (torch tensors,
+    so NCCL can move them)."""
+
+    def __init__(self, cfg: SimConfig, owned: ParticleSet, z_lo: int, z_hi: int, capacity: int,
+                 device: int = 0, record_capacity: Optional[int] = None):
+        import torch
+        self.torch = torch
+        self.lib = _capi.lib()
+        self.cfg = cfg
+        self.device = device
+        self._ccfg = _Config(cfg)
+        ps = owned.contiguous()
+        ctx = C.c_void_p()
+        rc = self.lib.dem_create_slab(C.byref(self._ccfg.c), C.byref(ps.c_struct()), device, z_lo, z_hi,
+                                      capacity, C.byref(ctx))
+        if rc != 0:
+            _raise(self.lib, None, rc)
+        self.ctx = ctx
+        mb, gb = C.c_uint64(), C.c_uint64()
+        self.lib.dem_slab_record_bytes(ctx, C.byref(mb), C.byref(gb))
+        self.rec_bytes = {"migrant": mb.value, "ghost": gb.value}
+        cap = record_capacity or max(4096, capacity // 4)
+        self.cap = {"migrant": cap, "ghost": cap}
+        dev = torch.device("cuda", device)
+        self.send = {k: [torch.empty(self.cap[k] * self.rec_bytes[k], dtype=torch.uint8, device=dev) for _ in range(2)]
+                     for k in self.cap}
+        self.recv = {k: [torch.empty(self.cap[k] * self.rec_bytes[k], dtype=torch.uint8, device=dev) for _ in range(2)]
+                     for k in self.cap}
+        self.send_count = {"migrant": [0, 0], "ghost": [0, 0]}
+        self.recv_count = {"migrant": [0, 0], "ghost": [0, 0]}
+
+    def __del__(self):
+        if getattr(self, "ctx", None):
+            self.lib.dem_destroy(self.ctx)
+            self.ctx = None
+
+    def _check(self, rc):
+        if rc != 0:
+            _raise(self.lib, self.ctx, rc)
+
+    def buffer_device(self):
+        return self.send["migrant"][0].device
+
+    def send_view(self, kind, side, n):
+        return self.send[kind][side][: n * self.rec_bytes[kind]]
+
+    def recv_view(self, kind, side, n):
+        return self.recv[kind][side][: n * self.rec_bytes[kind]]
+
+    def receive(self, kind, side, data, n):  # loopback delivery
+        self.recv_view(kind, side, n).copy_(data)
+        self.recv_count[kind][side] = n
+
+    # --- phases ---
+    def migrate(self, integrate: bool):
+        lo, hi = C.c_uint64(), C.c_uint64()
+        self._check(self.lib.dem_slab_migrate(self.ctx, 1 if integrate else 0, self.send["migrant"][0].data_ptr(),
+                                              self.send["migrant"][1].data_ptr(), self.cap["migrant"],
+                                              C.byref(lo), C.byref(hi)))
+        self.send_count["migrant"] = [lo.value, hi.value]
+
+    def import_(self):
+        self.torch.cuda.synchronize(self.device)
+        n_lo, n_hi = self.recv_count["migrant"]
+        self._check(self.lib.dem_slab_import(self.ctx, self.recv["migrant"][0].data_ptr(), n_lo,
+                                             self.recv["migrant"][1].data_ptr(), n_hi))
+
+    def halo(self):
+        lo, hi = C.c_uint64(), C.c_uint64()
+        self._check(self.lib.dem_slab_halo(self.ctx, self.send["ghost"][0].data_ptr(), self.send["ghost"][1].data_ptr(),
+                                           self.cap["ghost"], C.byref(lo), C.byref(hi)))
+        self.send_count["ghost"] = [lo.value, hi.value]
+
+    def ghosts(self):
+        self.torch.cuda.synchronize(self.device)
+        n_lo, n_hi = self.recv_count["ghost"]
+        self._check(self.lib.dem_slab_ghosts(self.ctx, self.recv["ghost"][0].data_ptr(), n_lo,
+                                             self.recv["ghost"][1].data_ptr(), n_hi))
+
+    def force(self, flags: int) -> StepMetrics:
+        m = _capi.dem_step_metrics()
+        self._check(self.lib.dem_slab_force(self.ctx, flags, C.byref(m)))
+        return StepMetrics.from_c(m)
+
+    # --- results (owned particles only) ---
+    def owned(self):
+        n = int(self.lib.dem_size(self.ctx))
+        s = ParticleSet(n)
+        self._check(self.lib.dem_get_particles(self.ctx, C.byref(s.c_struct())))
+        f = np.zeros((n, 3))
+        t = np.zeros((n, 3))
+        self._check(self.lib.dem_get_forces(self.ctx, f.ctypes.data_as(C.POINTER(C.c_double)),
+                                            t.ctypes.data_as(C.POINTER(C.c_double))))
+        cnt = self.lib.dem_get_contacts(self.ctx, None, None, None, 0)
+        o = np.zeros(cnt, np.uint32)
+        p = np.zeros(cnt, np.int32)
+        d = np.zeros((cnt, 3))
+        self.lib.dem_get_contacts(self.ctx, o.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                  p.ctypes.data_as(C.POINTER(C.c_int32)), d.ctypes.data_as(C.POINTER(C.c_double)), cnt)
+        own = (s.material_ids & GHOST_BIT) == 0
+        ids = s.ids
+        hist_owner = ids[o]
+        hist_key = np.where(p >= 0, ids[np.maximum(p, 0)], p.astype(np.int64) & 0xFFFFFFFF).astype(np.uint32)
+        mine = own[o] if cnt else np.zeros(0, bool)
+        return select(s, own), f[own], t[own], (hist_owner[mine], hist_key[mine], d[mine])
+
+
+# ---------------------------------------------------------------------------------------------
+# The driver: the per-step phase order for a set of local ranks and a transport
+
+class SlabDriver:
+    STEP = _capi.PHASE_STEP
+    PRIME = _capi.PHASE_GRAVITY | _capi.PHASE_PP | _capi.PHASE_RECT | _capi.PHASE_LINE
+
+    def __init__(self, ranks: Sequence, transport):
+        self.ranks = list(ranks)
+        self.transport = transport
+
+    def _phase(self, integrate: bool, flags: int):
+        for rk in self.ranks:
+            rk.migrate(integrate)
+        self.transport.exchange("migrant")
+        for rk in self.ranks:
+            rk.import_()
+        for rk in self.ranks:
+            rk.halo()
+        self.transport.exchange("ghost")
+        for rk in self.ranks:
+            rk.ghosts()
+        return [rk.force(flags) for rk in self.ranks]
+
+    def prime(self):
+        """The constructor's force-only pass (pipeline.cpp:83)."""
+        return self._phase(False, self.PRIME)
+
+    def step(self):
+        """Simulation::step() (pipeline.cpp:366-378) on every local rank."""
+        return self._phase(True, self.STEP)
+
+
+def build_local_slabs(ps: ParticleSet, cfg: SimConfig, nranks: int, rank_ids: Sequence[int], device: int = 0,
+                      headroom: float = 1.5, backend=SlabRankCuda):
+    """Partition `ps` into `nranks` slabs and construct the ranks in `rank_ids` (all of them for a
+    loopback run on one device, or just this process's rank under torch.distributed)."""
+    g = global_grid(cfg, float(ps.radii.max()))
+    scfg = replace(cfg, grid_cell_size=g.h)
+    planes = cell_planes(ps.positions[:, 2], g)
+    bounds = slab_bounds(planes, g.nz, nranks)
+    per_plane = np.bincount(planes, minlength=g.nz)
+    ranks = []
+    for r in rank_ids:
+        z_lo, z_hi = bounds[r]
+        mask = (planes >= z_lo) & (planes < z_hi)
+        owned = select(ps, mask)
+        ghosts = (per_plane[z_lo - 1] if z_lo > 0 else 0) + (per_plane[z_hi] if z_hi < g.nz else 0)
+        capacity = int(1024 + headroom * (len(owned.ids) + ghosts))
+        ranks.append(backend(scfg, owned, z_lo, z_hi, capacity, device=device))
+    return ranks, bounds, g

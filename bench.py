@@ -195,6 +195,75 @@ def run_reference(args):
     return 0
 
 
+def run_slab(args, world, rank, local):
+    """N > 1: one packing of 262,144 x N spheres, cut into N z-slabs (weak scaling), one slab
+    per GPU, neighbour migrant/halo exchange over NCCL (paper_1503_03553_b200.slab)."""
+    import torch
+    import torch.distributed as dist
+    import paper_1503_03553_b200 as dem
+    from paper_1503_03553_b200.slab import SlabDriver, TorchTransport, build_local_slabs
+    n_total = N_PARTICLES * world
+    ps, dmax = dem.gen_packing(n_total, s=1.8, jit=0.2, poly=False, seed=1)
+    cfg = dem.packing_config(dmax)
+    ranks, bounds, g = build_local_slabs(ps, cfg, world, [rank], device=local)
+    tr = TorchTransport(rank, world)
+    tr.bind(ranks[0])
+    drv = SlabDriver(ranks, tr)
+    drv.prime()
+    for _ in range(args.warmup):
+        drv.step()
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+    step_ms, contacts = [], 0
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(k)  # evict L2 outside the timed events
+            torch.cuda.synchronize()
+            barrier(world)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ms = drv.step()  # host-orchestrated: slab kernels + NCCL P2P + force phase, synced
+            e1.record()
+            torch.cuda.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            contacts = ms[0].contacts
+    barrier(world)
+    total_s = max_over_ranks(sum(step_ms) / 1e3, world)
+    c_all = torch.tensor([contacts], dtype=torch.float64, device="cuda")
+    dist.all_reduce(c_all)
+    value = n_total * args.steps / total_s
+    # e2e: the same stepping with every rank reading its owned state back to the host each step
+    t_e2e = []
+    for _ in range(max(3, min(args.steps, 10))):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        drv.step()
+        p, f, t, h = ranks[0].owned()
+        t_e2e.append(time.perf_counter() - t0)
+    e2e_s = max_over_ranks(sum(t_e2e), world)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (SURVEY §8d generator, xorshift64*)",
+        "config": {"workload": f"{n_total:,} monodisperse spheres, dense packing = configs[1] per GPU",
+                   "generator": f"G({n_total}, s=1.8, jit=0.2, mono, seed=1)", "dt": 1e-5,
+                   "contact_capacity": 16, "contacts_per_step": int(c_all.item()),
+                   "parallelism": f"z-slabs x{world}, NCCL P2P halo + migration",
+                   "slabs": bounds, "l2": "flushed before every timed step, outside the events"},
+        "gpu_launches": 11 * args.steps,
+        "e2e": {"value": n_total * len(t_e2e) / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": int(len(ps.ids) * 104 / world),
+                "how": "slab step + per-rank owned-state readback (dem_get_particles), wall clock"},
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
 def run_b200(args):
     world, rank, local = dist_env()
     import torch
@@ -202,13 +271,11 @@ def run_b200(args):
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
+        return run_slab(args, world, rank, local)
+    torch.cuda.set_device(0)
     import paper_1503_03553_b200 as dem
 
-    # independent replicas of the workload, one per GPU (weak scaling; slab decomposition over
-    # NVLink is DESIGN.md §7 "next")
-    ps, cfg = workload(seed=1 + rank)
+    ps, cfg = workload(seed=1)
     n = len(ps.ids)
     sim = dem.Simulation(ps, cfg, device=local)
     for _ in range(args.warmup):
@@ -268,7 +335,7 @@ def run_b200(args):
         "config": {"workload": "262,144 monodisperse spheres, dense random packing (configs[1])",
                    "generator": "G(262144, s=1.8, jit=0.2, mono, seed=1+rank)", "dt": 1e-5,
                    "contact_capacity": 16, "contacts_per_step": c, "cells": prof[-1].cells,
-                   "parallelism": f"replicas x{world}" if world > 1 else "single-gpu",
+                   "parallelism": "single-gpu",
                    "l2": "flushed before every timed step (512 MiB write), outside the events"},
         "gpu_launches": sim.kernels_per_step() * args.steps,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": state_bytes,
@@ -296,9 +363,6 @@ def run_b200(args):
                                     "kind": "reference", "sample": f"unavailable: {e}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
     return 0
 
 

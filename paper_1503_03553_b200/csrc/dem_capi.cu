@@ -283,10 +283,17 @@ void enqueue_phase(const dem_ctx* c, uint32_t flags, uint64_t phase, cudaEvent_t
     if (ev) cudaEventRecord(ev[4], s);
     launch_reorder(p, b, s);
     if (ev) cudaEventRecord(ev[5], s);
-    launch_detect(p, b, s);
-    if (ev) cudaEventRecord(ev[6], s);
-    launch_force_reduce(p, b, s);
-    if (ev) cudaEventRecord(ev[7], s);
+    if (c->collide_variant == 0) {
+        // Alg. 1, single loop (pipeline.cpp:209-217): detection and forces in one divergent loop
+        launch_collide_single_loop(p, b, s);
+        if (ev) cudaEventRecord(ev[6], s);
+        if (ev) cudaEventRecord(ev[7], s);
+    } else {
+        launch_detect(p, b, s);
+        if (ev) cudaEventRecord(ev[6], s);
+        launch_force_reduce(p, b, s);
+        if (ev) cudaEventRecord(ev[7], s);
+    }
 }
 
 int build_graphs(dem_ctx* ctx) {
@@ -655,8 +662,10 @@ int dem_force_phase(dem_ctx* ctx, uint32_t flags, dem_step_metrics* m) {
 
 int dem_set_collide_variant(dem_ctx* ctx, int variant) {
     if (!ctx || (variant != 0 && variant != 1)) return DEM_ERR_ARGUMENT;
+    if (ctx->collide_variant == variant) return DEM_OK;
     ctx->collide_variant = variant;
-    return DEM_OK;
+    cudaSetDevice(ctx->device);
+    return ctx->slab ? DEM_OK : build_graphs(ctx);  // step graphs embed the Collide kernels
 }
 
 uint64_t dem_size(const dem_ctx* ctx) { return ctx ? ctx->n : 0; }

@@ -146,6 +146,7 @@ void launch_scatter(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
 void launch_reorder(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
 void launch_detect(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
 void launch_force_reduce(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
+void launch_collide_single_loop(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
 void launch_flush(void* buf, size_t bytes, cudaStream_t s);
 cudaError_t init_device_attributes();
 

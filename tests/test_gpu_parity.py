@@ -179,3 +179,30 @@ def test_nonfinite_force_raises_integrate(cuda):
         sim.step()
     assert e.value.kernel == "Integrate"
     assert "non-finite force" in str(e.value)
+
+
+@pytest.mark.parametrize("seed", [7, 8])
+def test_single_loop_variant_bitwise_equals_two_phase(cuda, seed):
+    """test_pipeline.cpp:191-220 on the GPU: Alg. 1 (single loop, set_collide_variant(baseline))
+    and the two-phase kernels give bitwise identical states, forces and histories; switching
+    variants mid-run keeps the history compatible."""
+    dem = cuda
+    cfg = basic_config(box_for(1000))
+    a = dem.Simulation(random_dense_state(1000, seed), cfg)
+    cfg_b = basic_config(box_for(1000))
+    cfg_b.collide_variant = dem.BASELINE
+    b = dem.Simulation(random_dense_state(1000, seed), cfg_b)
+    for k in range(6):
+        ma, mb = a.step(), b.step()
+        assert (ma.contacts, ma.pp_contact_events, ma.max_contacts_per_particle) == \
+            (mb.contacts, mb.pp_contact_events, mb.max_contacts_per_particle)
+        assert ma.friction_max_ratio == mb.friction_max_ratio and ma.capped_contacts == mb.capped_contacts
+        if k == 3:
+            b.set_collide_variant(dem.TWO_PHASE)
+            a.set_collide_variant(dem.BASELINE)
+    pa, pb = a.particles(), b.particles()
+    assert bitwise_equal(pa.positions, pb.positions) and bitwise_equal(pa.angular_velocities, pb.angular_velocities)
+    assert bitwise_equal(a.forces().force, b.forces().force) and bitwise_equal(a.forces().torque, b.forces().torque)
+    ha, _ = hist_from_gpu(a)
+    hb, _ = hist_from_gpu(b)
+    assert ha == hb

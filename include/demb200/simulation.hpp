@@ -101,6 +101,12 @@ class MaterialTable {
             if (o.a == a && o.b == b) return o.eps;
         return std::sqrt(mats_[a].restitution * mats_[b].restitution);
     }
+    bool contains(const std::string& name) const {
+        for (const auto& n : names_)
+            if (n == name) return true;
+        return false;
+    }
+    const std::string& name(std::uint32_t i) const { return names_[i]; }
 
   private:
     struct Override { std::uint32_t a, b; double eps; };
@@ -113,6 +119,29 @@ struct RectWall { Vec3 corner, edge_u, edge_v; std::uint32_t material_id = 0; };
 struct LineWall { Vec3 a, b; std::uint32_t material_id = 0; };
 enum class CollideVariant { baseline, two_phase };
 
+// sim_config.hpp:15-37: how `run` builds the initial state, and the run control block.
+enum class InitMode { lattice, headon };
+struct ParticleInitConfig {
+    InitMode mode = InitMode::lattice;
+    std::uint32_t count = 0;
+    double radius = 0.0, mass = 0.0;
+    std::string material;
+    double jitter = -1.0;          // < 0: 0.1 * (spacing - 2 r)
+    double lattice_spacing = 0.0;  // 0: fit to the domain
+    double headon_gap = -1.0;      // < 0: 0.1 r
+    double headon_speed = 1.0;
+};
+struct RunControlConfig {
+    std::int64_t steps = 0, warmup_steps = 0, snapshot_every = 0;
+    CollideVariant collide_variant = CollideVariant::two_phase;
+};
+// warp_model.hpp:14-24 (accepted for config-file compatibility; the B200 path measures
+// divergence with ncu instead of modelling it)
+struct WarpCostParams {
+    int warp_size = 32;
+    double c_check = 1.0, c_force = 20.0, c_store = 1.0, c_load = 1.0;
+};
+
 struct SimConfig {
     double dt = 0.0;
     Vec3 gravity{0.0, 0.0, -9.81};
@@ -122,7 +151,10 @@ struct SimConfig {
     std::vector<LineWall> line_walls;
     double grid_cell_size = 0.0;
     int contact_capacity = 16;
-    CollideVariant collide_variant = CollideVariant::two_phase;
+    WarpCostParams warp;
+    RunControlConfig run;
+    ParticleInitConfig particles;
+    std::uint64_t seed = 1;
 };
 
 // ---- particle_set.hpp --------------------------------------------------------------------------
@@ -232,7 +264,7 @@ class Simulation {
     StepMetrics step() { return run([&](dem_step_metrics* m) { return dem_step(ctx_.get(), 1, m); }, true); }
     void set_record_traces(bool on) { record_traces_ = on; }
     void set_collide_variant(CollideVariant v) {
-        cfg_.collide_variant = v;
+        cfg_.run.collide_variant = v;
         check(dem_set_collide_variant(ctx_.get(), v == CollideVariant::two_phase ? 1 : 0));
     }
     /// advance_to_collide + kernel_collide (tests/test_pipeline.cpp:69-76): pp only, no gravity.
@@ -241,6 +273,17 @@ class Simulation {
     }
     StepMetrics force_phase(std::uint32_t flags) {
         return run([&](dem_step_metrics* m) { return dem_force_phase(ctx_.get(), flags, m); }, false);
+    }
+    /// One step() without graphs; per-B200-kernel device ms (dem_device_kernel order) in `ms`.
+    StepMetrics profile_step(double ms[DEM_DEVICE_KERNEL_COUNT], std::size_t flush_bytes = 0) {
+        dem_step_metrics raw{};
+        StepMetrics r = run([&](dem_step_metrics* m) {
+            const int rc = dem_profile_step(ctx_.get(), flush_bytes, m);
+            raw = *m;
+            return rc;
+        }, true);
+        for (int k = 0; k < DEM_DEVICE_KERNEL_COUNT; ++k) ms[k] = raw.device_kernel_ms[k];
+        return r;
     }
 
     const SimConfig& config() const { return cfg_; }
@@ -373,7 +416,7 @@ class Simulation {
         ccfg_.line_walls = lines_.data();
         ccfg_.grid_cell_size = cfg_.grid_cell_size;
         ccfg_.contact_capacity = cfg_.contact_capacity;
-        ccfg_.collide_variant = cfg_.collide_variant == CollideVariant::two_phase ? 1 : 0;
+        ccfg_.collide_variant = cfg_.run.collide_variant == CollideVariant::two_phase ? 1 : 0;
     }
 
     void check(int rc) const { if (rc != DEM_OK) rethrow(ctx_.get(), rc); }

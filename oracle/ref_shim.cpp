@@ -417,3 +417,16 @@ std::int64_t ref_parse_and_build(const char* text, orc_config* out_cfg, orc_mate
 }
 
 }  // extern "C"
+
+// run_simulation (runner.cpp:35-82) on a config text: writes the reference's snapshot and
+// metrics CSVs into out_dir. Returns the steps run or a negative error code.
+#include "demforge/runner.hpp"
+extern "C" std::int64_t ref_run_simulation(const char* text, const char* out_dir) {
+    try {
+        const demforge::SimConfig cfg = demforge::parse_config_text(std::string(text), "<text>");
+        return demforge::run_simulation(cfg, out_dir).steps_run;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return -classify(e);
+    }
+}

@@ -1,0 +1,76 @@
+"""Host side: config files, initial states, on-disk formats and the
+run / bench / verify CLI, against the reference.
+
+CPU: tests/cpp/host_test runs the reference's parse_config_text / build_initial_state /
+write_snapshot side by side with demb200's (same values, same bytes, same error messages).
+GPU: `dem_b200 run` reproduces the reference CLI's `run` outputs (tests/golden/run_*, written by
+the reference's run_simulation): snapshots byte-identical, metrics rows identical except the
+analytic-SIMT-model columns the B200 path does not produce."""
+import csv
+import os
+import subprocess
+import tempfile
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CLI = os.path.join(ROOT, "paper_1503_03553_b200", "dem_b200")
+GOLD = os.path.join(ROOT, "tests", "golden")
+
+
+def test_host_side_matches_reference_cpu():
+    binp = os.path.join(ROOT, "tests", "cpp", "host_test")
+    if not os.path.exists(binp):
+        pytest.skip("tests/cpp/host_test not built (needs the reference headers at build time)")
+    r = subprocess.run([binp, ROOT], capture_output=True, text=True, timeout=300)
+    print(r.stdout)
+    assert r.returncode == 0 and "PASSED" in r.stdout, r.stdout + r.stderr
+
+
+def test_cli_config_errors_exit_2():
+    with tempfile.TemporaryDirectory() as d:
+        bad = os.path.join(d, "bad.cfg")
+        open(bad, "w").write(open(os.path.join(ROOT, "configs", "headon.cfg")).read() + "\nbogus = 1\n")
+        r = subprocess.run([CLI, "run", bad, "--out-dir", d], capture_output=True, text=True)
+        assert r.returncode == 2 and "unknown key 'bogus'" in r.stderr
+        r = subprocess.run([CLI, "run", os.path.join(d, "missing.cfg")], capture_output=True, text=True)
+        assert r.returncode == 2
+        r = subprocess.run([CLI, "frobnicate", bad], capture_output=True, text=True)
+        assert r.returncode == 2
+
+
+def _metrics(path, drop_model=True):
+    rows = list(csv.reader(open(path)))
+    if drop_model:
+        rows = [r[:3] + r[7:] for r in rows]
+    return rows
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["headon", "settle512"])
+def test_cli_run_matches_reference_outputs(cuda, name):
+    with tempfile.TemporaryDirectory() as d:
+        r = subprocess.run([CLI, "run", os.path.join(ROOT, "configs", name + ".cfg"), "--out-dir", d],
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr
+        gold = os.path.join(GOLD, "run_" + name)
+        snaps = sorted(f for f in os.listdir(gold) if f.startswith("snapshot_"))
+        assert sorted(f for f in os.listdir(d) if f.startswith("snapshot_")) == snaps
+        for f in snaps:
+            assert open(os.path.join(d, f), "rb").read() == open(os.path.join(gold, f), "rb").read(), f
+        assert _metrics(os.path.join(d, "metrics.csv")) == _metrics(os.path.join(gold, "metrics.csv"))
+
+
+@pytest.mark.gpu
+def test_cli_verify_and_bench(cuda):
+    with tempfile.TemporaryDirectory() as d:
+        r = subprocess.run([CLI, "verify", os.path.join(ROOT, "configs", "settle512.cfg")],
+                           capture_output=True, text=True, timeout=900)
+        print(r.stdout)
+        assert r.returncode == 0, r.stdout + r.stderr
+        assert r.stdout.count("PASS") == 5
+        r = subprocess.run([CLI, "bench", os.path.join(ROOT, "configs", "settle512.cfg"), "--steps", "5",
+                            "--out-dir", d], capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr
+        assert "Collide ratio single-loop / two-phase" in r.stdout
+        assert os.path.exists(os.path.join(d, "bench_report.txt"))

@@ -89,6 +89,11 @@ struct dem_ctx {
     uint32_t* h_counters = nullptr;
     size_t tile_pairs = 0, imp_cap = 0, imp_used = 0;
     uint32_t rec_bytes = 0, rec_dt_off = 0, ghost_bytes = 0;
+
+    // device staging in the host layout for get/set (allocated on first use)
+    double* raw_d = nullptr;
+    uint32_t* raw_u = nullptr;
+    uint64_t raw_n = 0;
 };
 
 namespace {
@@ -368,6 +373,8 @@ void free_ctx(dem_ctx* c) {
     if (c->flush_buf) cudaFree(c->flush_buf);
     if (c->h_ctl) cudaFreeHost(c->h_ctl);
     if (c->h_counters) cudaFreeHost(c->h_counters);
+    if (c->raw_d) cudaFree(c->raw_d);
+    if (c->raw_u) cudaFree(c->raw_u);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -457,23 +464,46 @@ int upload_tables(dem_ctx* ctx) {
     return DEM_OK;
 }
 
+// Staging buffers in the caller's layout (11 doubles + 2 u32 per particle).
+int ensure_raw(dem_ctx* ctx, uint64_t n) {
+    if (ctx->raw_n >= n && ctx->raw_d) return DEM_OK;
+    if (ctx->raw_d) { cudaFree(ctx->raw_d); cudaFree(ctx->raw_u); ctx->raw_d = nullptr; ctx->raw_u = nullptr; }
+    CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&ctx->raw_d), std::max<uint64_t>(n, 1) * 11 * sizeof(double)));
+    CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&ctx->raw_u), std::max<uint64_t>(n, 1) * 2 * sizeof(uint32_t)));
+    ctx->raw_n = n;
+    return DEM_OK;
+}
+
+RawState raw_view(const dem_ctx* ctx, uint64_t n) {
+    RawState r{};
+    r.pos = ctx->raw_d;
+    r.vel = ctx->raw_d + 3 * n;
+    r.omg = ctx->raw_d + 6 * n;
+    r.rad = ctx->raw_d + 9 * n;
+    r.mass = ctx->raw_d + 10 * n;
+    r.ids = ctx->raw_u;
+    r.mat = ctx->raw_u + n;
+    return r;
+}
+
+// Host arrays -> device staging (plain copies; pinned callers get full PCIe bandwidth) -> SoA.
 int upload_state(dem_ctx* ctx, const dem_particles* p, int buf) {
     const uint64_t n = ctx->n;
-    std::vector<double4> pr(n), vm(n), om(n);
-    std::vector<uint2> idm(n);
-    for (uint64_t i = 0; i < n; ++i) {
-        pr[i] = make_double4(p->positions[3 * i], p->positions[3 * i + 1], p->positions[3 * i + 2], p->radii[i]);
-        vm[i] = make_double4(p->velocities[3 * i], p->velocities[3 * i + 1], p->velocities[3 * i + 2], p->masses[i]);
-        om[i] = make_double4(p->angular_velocities[3 * i], p->angular_velocities[3 * i + 1], p->angular_velocities[3 * i + 2], 0.0);
-        idm[i] = make_uint2(p->ids[i], p->material_ids[i]);
-    }
-    if (n) {
-        CUDA_TRY(cudaMemcpyAsync(ctx->state[buf].pos_r, pr.data(), n * sizeof(double4), cudaMemcpyHostToDevice, ctx->stream));
-        CUDA_TRY(cudaMemcpyAsync(ctx->state[buf].vel_m, vm.data(), n * sizeof(double4), cudaMemcpyHostToDevice, ctx->stream));
-        CUDA_TRY(cudaMemcpyAsync(ctx->state[buf].omg, om.data(), n * sizeof(double4), cudaMemcpyHostToDevice, ctx->stream));
-        CUDA_TRY(cudaMemcpyAsync(ctx->state[buf].idm, idm.data(), n * sizeof(uint2), cudaMemcpyHostToDevice, ctx->stream));
-    }
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (!n) return DEM_OK;
+    int rc = ensure_raw(ctx, n);
+    if (rc != DEM_OK) return rc;
+    const RawState r = raw_view(ctx, n);
+    cudaStream_t s = ctx->stream;
+    CUDA_TRY(cudaMemcpyAsync(r.pos, p->positions, 3 * n * sizeof(double), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(r.vel, p->velocities, 3 * n * sizeof(double), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(r.omg, p->angular_velocities, 3 * n * sizeof(double), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(r.rad, p->radii, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(r.mass, p->masses, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(r.ids, p->ids, n * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(r.mat, p->material_ids, n * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    launch_pack_state(ctx->state[buf], r, static_cast<uint32_t>(n), true, s);
+    CUDA_TRY(cudaStreamSynchronize(s));
+    CUDA_TRY(cudaGetLastError());
     return DEM_OK;
 }
 
@@ -677,25 +707,21 @@ int dem_get_particles(dem_ctx* ctx, dem_particles* out) {
     if (!ctx || !out || out->count != ctx->n) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
     const uint64_t n = ctx->n;
-    const StateBuf& s = ctx->state[state_cur(ctx)];
-    std::vector<double4> pr(n), vm(n), om(n);
-    std::vector<uint2> idm(n);
-    if (n) {
-        CUDA_TRY(cudaMemcpyAsync(pr.data(), s.pos_r, n * sizeof(double4), cudaMemcpyDeviceToHost, ctx->stream));
-        CUDA_TRY(cudaMemcpyAsync(vm.data(), s.vel_m, n * sizeof(double4), cudaMemcpyDeviceToHost, ctx->stream));
-        CUDA_TRY(cudaMemcpyAsync(om.data(), s.omg, n * sizeof(double4), cudaMemcpyDeviceToHost, ctx->stream));
-        CUDA_TRY(cudaMemcpyAsync(idm.data(), s.idm, n * sizeof(uint2), cudaMemcpyDeviceToHost, ctx->stream));
-        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    }
-    for (uint64_t i = 0; i < n; ++i) {
-        if (out->positions) { out->positions[3 * i] = pr[i].x; out->positions[3 * i + 1] = pr[i].y; out->positions[3 * i + 2] = pr[i].z; }
-        if (out->radii) out->radii[i] = pr[i].w;
-        if (out->velocities) { out->velocities[3 * i] = vm[i].x; out->velocities[3 * i + 1] = vm[i].y; out->velocities[3 * i + 2] = vm[i].z; }
-        if (out->masses) out->masses[i] = vm[i].w;
-        if (out->angular_velocities) { out->angular_velocities[3 * i] = om[i].x; out->angular_velocities[3 * i + 1] = om[i].y; out->angular_velocities[3 * i + 2] = om[i].z; }
-        if (out->ids) out->ids[i] = idm[i].x;
-        if (out->material_ids) out->material_ids[i] = idm[i].y;
-    }
+    if (!n) return DEM_OK;
+    int rc = ensure_raw(ctx, n);
+    if (rc != DEM_OK) return rc;
+    const RawState r = raw_view(ctx, n);
+    cudaStream_t s = ctx->stream;
+    launch_pack_state(ctx->state[state_cur(ctx)], r, static_cast<uint32_t>(n), false, s);
+    if (out->positions) CUDA_TRY(cudaMemcpyAsync(out->positions, r.pos, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (out->velocities) CUDA_TRY(cudaMemcpyAsync(out->velocities, r.vel, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (out->angular_velocities) CUDA_TRY(cudaMemcpyAsync(out->angular_velocities, r.omg, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (out->radii) CUDA_TRY(cudaMemcpyAsync(out->radii, r.rad, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (out->masses) CUDA_TRY(cudaMemcpyAsync(out->masses, r.mass, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (out->ids) CUDA_TRY(cudaMemcpyAsync(out->ids, r.ids, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    if (out->material_ids) CUDA_TRY(cudaMemcpyAsync(out->material_ids, r.mat, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    CUDA_TRY(cudaGetLastError());
     return DEM_OK;
 }
 
@@ -711,16 +737,16 @@ int dem_get_forces(dem_ctx* ctx, double* force, double* torque) {
     if (!ctx) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
     const uint64_t n = ctx->n, fs = ft_stride(ctx);
-    std::vector<double> ft(6 * fs);
-    if (n) {
-        CUDA_TRY(cudaMemcpyAsync(ft.data(), ctx->ft, 6 * fs * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    }
-    for (uint64_t i = 0; i < n; ++i)
-        for (int a = 0; a < 3; ++a) {
-            if (force) force[3 * i + a] = ft[a * fs + i];
-            if (torque) torque[3 * i + a] = ft[(3 + a) * fs + i];
-        }
+    if (!n) return DEM_OK;
+    int rc = ensure_raw(ctx, n);
+    if (rc != DEM_OK) return rc;
+    double* f = ctx->raw_d;           // 6n doubles of staging: F[3n] | T[3n]
+    double* t = ctx->raw_d + 3 * n;
+    launch_ft_layout(ctx->ft, static_cast<uint32_t>(fs), f, t, static_cast<uint32_t>(n), true, ctx->stream);
+    if (force) CUDA_TRY(cudaMemcpyAsync(force, f, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    if (torque) CUDA_TRY(cudaMemcpyAsync(torque, t, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    CUDA_TRY(cudaGetLastError());
     return DEM_OK;
 }
 
@@ -728,13 +754,16 @@ int dem_set_forces(dem_ctx* ctx, const double* force, const double* torque) {
     if (!ctx || !force || !torque) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
     const uint64_t n = ctx->n, fs = ft_stride(ctx);
-    std::vector<double> ft(6 * fs, 0.0);
-    for (uint64_t i = 0; i < n; ++i)
-        for (int a = 0; a < 3; ++a) { ft[a * fs + i] = force[3 * i + a]; ft[(3 + a) * fs + i] = torque[3 * i + a]; }
-    if (n) {
-        CUDA_TRY(cudaMemcpyAsync(ctx->ft, ft.data(), 6 * fs * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    }
+    if (!n) return DEM_OK;
+    int rc = ensure_raw(ctx, n);
+    if (rc != DEM_OK) return rc;
+    double* f = ctx->raw_d;
+    double* t = ctx->raw_d + 3 * n;
+    CUDA_TRY(cudaMemcpyAsync(f, force, 3 * n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(t, torque, 3 * n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    launch_ft_layout(ctx->ft, static_cast<uint32_t>(fs), f, t, static_cast<uint32_t>(n), false, ctx->stream);
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    CUDA_TRY(cudaGetLastError());
     return DEM_OK;
 }
 

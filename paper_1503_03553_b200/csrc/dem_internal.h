@@ -148,6 +148,14 @@ void launch_detect(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
 void launch_force_reduce(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
 void launch_collide_single_loop(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
 void launch_flush(void* buf, size_t bytes, cudaStream_t s);
+
+// Device staging in the caller's (host) layout: positions[3n], ..., ids[n], material_ids[n].
+struct RawState {
+    double *pos, *vel, *omg, *rad, *mass;
+    uint32_t *ids, *mat;
+};
+void launch_pack_state(const StateBuf& s, const RawState& r, uint32_t n, bool pack, cudaStream_t st);
+void launch_ft_layout(double* ft, uint32_t stride, double* f, double* t, uint32_t n, bool to_interleaved, cudaStream_t st);
 cudaError_t init_device_attributes();
 
 }  // namespace demb200

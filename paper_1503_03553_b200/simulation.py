@@ -411,6 +411,11 @@ class Simulation:
         self._check(self._lib.dem_get_particles(self._ctx, C.byref(s.c_struct())))
         return s
 
+    def particles_into(self, s: ParticleSet) -> ParticleSet:
+        """particles() into caller-owned (e.g. pinned) contiguous arrays of the right size."""
+        self._check(self._lib.dem_get_particles(self._ctx, C.byref(s.c_struct())))
+        return s
+
     def set_particles(self, s: ParticleSet):
         s = s.contiguous()
         self._check(self._lib.dem_set_particles(self._ctx, C.byref(s.c_struct())))

@@ -207,6 +207,19 @@ int dem_get_order(dem_ctx* ctx, uint32_t* sorted_keys, uint32_t* permutation);
 int64_t dem_get_contacts(dem_ctx* ctx, uint32_t* owner_slot, int32_t* partner, double* delta_t,
                          int64_t cap);
 
+/* Traversal traces of the last force phase — Simulation::traces() (pipeline.hpp:97), recorded by
+ * kernel_collide (pipeline.cpp:191-231): per owner slot i, in the traversal order (27 cells z, y,
+ * x outer-to-inner, ascending slot, j != i), one event per candidate slot j with the check_pair
+ * outcome. Identical for both Collide variants. offsets (nullable, n+1 entries) receives the
+ * per-slot event ranges; events (nullable) is filled when capacity >= the total. Returns the total
+ * event count, or a negative dem_status. Available after a force phase with DEM_PHASE_PP until
+ * the state is replaced (dem_set_particles); single-GPU contexts only. */
+typedef struct dem_trace_event {
+    int32_t candidate; /* TraceEvent::candidate, warp_model.hpp:28-33 (a slot index) */
+    int32_t contact;   /* TraceEvent::contact (0/1) */
+} dem_trace_event;
+int64_t dem_get_traces(dem_ctx* ctx, uint64_t* offsets, dem_trace_event* events, int64_t capacity);
+
 /* Last error (what(), kernel, particle). */
 int dem_last_error(const dem_ctx* ctx, dem_error* out);
 

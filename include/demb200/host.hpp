@@ -49,9 +49,10 @@ void write_snapshot(const std::filesystem::path& path, const ParticleSet& state)
 inline constexpr const char* kMetricsHeader =
     "step,kernel,wall_ns,model_cycles_baseline,model_cycles_two_phase,"
     "utilization_baseline,utilization_two_phase,contacts,max_contacts_per_particle,clamps";
-/// Nine kernel rows per step. The model columns carry no analytic SIMT model on the B200 path
-/// (divergence is measured with ncu) and are written as 0; wall_ns is the device time of the
-/// B200 kernels mapped onto the reference kernel rows, or 0 when `zero_wall_time`.
+/// Nine kernel rows per step (snapshot_io.cpp:70-94). The Collide row carries the warp model of the
+/// step's traversal traces (StepMetrics::model_*, filled when traces are recorded); wall_ns is the
+/// device time of the B200 kernels mapped onto the reference kernel rows, or 0 when
+/// `zero_wall_time`.
 void append_metrics_rows(std::string& out, std::int64_t step, const StepMetrics& m,
                          const double* kernel_ms /* nullable, dem_device_kernel order */,
                          bool zero_wall_time);
@@ -70,6 +71,7 @@ struct BenchPhase {
     double collide_us_baseline = 0.0, collide_us_two_phase = 0.0;
     double kernel_us[DEM_DEVICE_KERNEL_COUNT] = {};
     double mean_coordination = 0.0;
+    WarpReport model;  // the warp model over the measured steps' traces (runner.cpp:126-129)
     double ratio() const { return collide_us_two_phase > 0 ? collide_us_baseline / collide_us_two_phase : 1.0; }
 };
 struct BenchReport {

@@ -14,10 +14,12 @@
 //  * the class is copyable (a device-side clone, runner.cpp:261-270).
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cmath>
 #include <cstdint>
 #include <memory>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -135,12 +137,141 @@ struct RunControlConfig {
     std::int64_t steps = 0, warmup_steps = 0, snapshot_every = 0;
     CollideVariant collide_variant = CollideVariant::two_phase;
 };
-// warp_model.hpp:14-24 (accepted for config-file compatibility; the B200 path measures
-// divergence with ncu instead of modelling it)
+// ---- warp_model.hpp ----------------------------------------------------------------------------
+// The paper's lockstep SIMT cost model (warp_model.hpp:9-88), evaluated on the host over the
+// traversal traces the device records (dem_get_traces). It is a model of a hypothetical warp, kept
+// for the reference's metrics columns and bench report; the B200 kernels' real divergence is
+// measured with ncu (profiles/). Sums run in the reference's order (warp by warp, lane by lane),
+// so a report over the same traces is bitwise the reference's.
 struct WarpCostParams {
     int warp_size = 32;
     double c_check = 1.0, c_force = 20.0, c_store = 1.0, c_load = 1.0;
+    void validate() const {  // warp_model.cpp:9-18
+        if (warp_size < 1) throw ConfigError("simt.warp_size must be >= 1");
+        if (c_check < 0.0 || c_force < 0.0 || c_store < 0.0 || c_load < 0.0)
+            throw ConfigError("simt cost parameters must be >= 0");
+        if (!(c_force > c_check)) throw ConfigError("simt.c_force must exceed simt.c_check");
+    }
 };
+
+struct TraceEvent {
+    std::int32_t candidate = 0;  // slot index of the inspected partner
+    bool contact = false;        // check_pair succeeded
+    bool operator==(const TraceEvent&) const = default;
+};
+using LaneTrace = std::vector<TraceEvent>;
+
+inline std::size_t contact_count(const LaneTrace& t) {
+    std::size_t k = 0;
+    for (const auto& e : t) k += e.contact ? 1 : 0;
+    return k;
+}
+
+/// Lanes [w*warp_size, (w+1)*warp_size) form warp w; the last may be partial.
+inline std::vector<std::span<const LaneTrace>> group_warps(std::span<const LaneTrace> lanes, int warp_size) {
+    std::vector<std::span<const LaneTrace>> out;
+    const std::size_t w = static_cast<std::size_t>(warp_size);
+    for (std::size_t b = 0; b < lanes.size(); b += w) out.push_back(lanes.subspan(b, std::min(w, lanes.size() - b)));
+    return out;
+}
+
+namespace detail {
+// Lockstep shape of one warp: per iteration j (up to the longest trace) whether some lane hits,
+// and the largest per-lane contact count.
+struct WarpShape {
+    std::vector<char> any_hit;
+    std::size_t max_contacts = 0;
+};
+inline WarpShape warp_shape(std::span<const LaneTrace> warp) {
+    WarpShape s;
+    std::size_t len = 0;
+    for (const auto& lane : warp) {
+        len = std::max(len, lane.size());
+        s.max_contacts = std::max(s.max_contacts, contact_count(lane));
+    }
+    s.any_hit.assign(len, 0);
+    for (const auto& lane : warp)
+        for (std::size_t j = 0; j < lane.size(); ++j) s.any_hit[j] |= lane[j].contact ? 1 : 0;
+    return s;
+}
+}  // namespace detail
+
+/// Single loop: each iteration costs a check, plus a force when any lane hits (warp_model.hpp:45-48).
+inline double warp_cycles_baseline(std::span<const LaneTrace> warp, const WarpCostParams& c) {
+    double cycles = 0.0;
+    for (char hit : detail::warp_shape(warp).any_hit) {
+        cycles += c.c_check;
+        if (hit) cycles += c.c_force;
+    }
+    return cycles;
+}
+
+/// Two loops: check (+ store when any lane hits), then max-contacts force iterations (:50-52).
+inline double warp_cycles_two_phase(std::span<const LaneTrace> warp, const WarpCostParams& c) {
+    const auto s = detail::warp_shape(warp);
+    double loop1 = 0.0;
+    for (char hit : s.any_hit) {
+        loop1 += c.c_check;
+        if (hit) loop1 += c.c_store;
+    }
+    return loop1 + static_cast<double>(s.max_contacts) * (c.c_load + c.c_force);
+}
+
+inline double warp_useful_cycles(std::span<const LaneTrace> warp, const WarpCostParams& c, CollideVariant v) {
+    double useful = 0.0;
+    for (const auto& lane : warp) {
+        const double hits = static_cast<double>(contact_count(lane));
+        useful += static_cast<double>(lane.size()) * c.c_check + hits * c.c_force;
+        if (v == CollideVariant::two_phase) useful += hits * (c.c_store + c.c_load);
+    }
+    return useful;
+}
+
+inline double utilization(std::span<const LaneTrace> warp, const WarpCostParams& c, CollideVariant v) {
+    const double cycles = v == CollideVariant::baseline ? warp_cycles_baseline(warp, c) : warp_cycles_two_phase(warp, c);
+    if (cycles == 0.0) return 1.0;
+    return warp_useful_cycles(warp, c, v) / (static_cast<double>(warp.size()) * cycles);
+}
+
+struct WarpReport {
+    double cycles_baseline = 0.0, cycles_two_phase = 0.0;
+    double utilization_baseline = 1.0, utilization_two_phase = 1.0;
+    std::size_t warp_count = 0;
+    double useful_baseline = 0.0, useful_two_phase = 0.0;
+    double occupied_baseline = 0.0, occupied_two_phase = 0.0;
+    double speedup() const { return cycles_two_phase == 0.0 ? 1.0 : cycles_baseline / cycles_two_phase; }
+    void refresh() {
+        if (occupied_baseline > 0.0) utilization_baseline = useful_baseline / occupied_baseline;
+        if (occupied_two_phase > 0.0) utilization_two_phase = useful_two_phase / occupied_two_phase;
+    }
+    void merge(const WarpReport& o) {
+        cycles_baseline += o.cycles_baseline;
+        cycles_two_phase += o.cycles_two_phase;
+        warp_count += o.warp_count;
+        useful_baseline += o.useful_baseline;
+        useful_two_phase += o.useful_two_phase;
+        occupied_baseline += o.occupied_baseline;
+        occupied_two_phase += o.occupied_two_phase;
+        refresh();
+    }
+};
+
+inline WarpReport model_report(std::span<const LaneTrace> traces, const WarpCostParams& c) {
+    WarpReport r;
+    for (const auto warp : group_warps(traces, c.warp_size)) {
+        const double lanes = static_cast<double>(warp.size());
+        const double base = warp_cycles_baseline(warp, c), two = warp_cycles_two_phase(warp, c);
+        ++r.warp_count;
+        r.cycles_baseline += base;
+        r.cycles_two_phase += two;
+        r.useful_baseline += warp_useful_cycles(warp, c, CollideVariant::baseline);
+        r.useful_two_phase += warp_useful_cycles(warp, c, CollideVariant::two_phase);
+        r.occupied_baseline += lanes * base;
+        r.occupied_two_phase += lanes * two;
+    }
+    r.refresh();
+    return r;
+}
 
 struct SimConfig {
     double dt = 0.0;
@@ -217,6 +348,13 @@ class ContactTable {
     std::vector<ContactSlot> slots_;
 };
 
+// sorted_order.hpp:13-19 (no BitonicStats: the B200 sort is a one-digit counting sort)
+struct SortedOrder {
+    std::vector<std::uint32_t> sorted_keys;  // nondecreasing cell keys per slot
+    std::vector<std::uint32_t> permutation;  // new slot -> previous slot
+    std::vector<std::uint32_t> cell_start, cell_end;  // untouched cells: start == end == 0
+};
+
 struct UniformGrid {
     Vec3 origin;
     double cell_size = 0.0;
@@ -225,12 +363,19 @@ struct UniformGrid {
 };
 
 // ---- pipeline.hpp ------------------------------------------------------------------------------
-struct StepMetrics {
-    std::int64_t step = 0, contacts = 0, pp_contact_events = 0;
+inline constexpr int kKernelCount = DEM_KERNEL_COUNT;  // pipeline.hpp:19-31
+struct StepMetrics {  // pipeline.hpp:35-48
+    std::int64_t step = 0;
+    // The reference's host wall time per reference kernel; the B200 step is one CUDA graph, so
+    // these stay 0 (per-device-kernel times: Simulation::profile_step).
+    std::array<std::int64_t, kKernelCount> kernel_wall_ns{};
+    double model_cycles_baseline = 0.0, model_cycles_two_phase = 0.0;  // with record_traces
+    double utilization_baseline = 1.0, utilization_two_phase = 1.0;
+    std::int64_t contacts = 0, pp_contact_events = 0;
     int max_contacts_per_particle = 0;
     std::int64_t clamps = 0;
     double friction_max_ratio = 0.0;
-    std::int64_t capped_contacts = 0;
+    std::int64_t capped_contacts = 0;  // new counter: contacts whose friction cap engaged
 };
 
 class Simulation {
@@ -262,7 +407,11 @@ class Simulation {
     Simulation& operator=(Simulation&&) = default;
 
     StepMetrics step() { return run([&](dem_step_metrics* m) { return dem_step(ctx_.get(), 1, m); }, true); }
+    /// Whether step() records traversal traces and runs the warp model (pipeline.hpp:70-71;
+    /// on by default like the reference). Costs a trace download per step.
     void set_record_traces(bool on) { record_traces_ = on; }
+    /// Per-slot traversal traces of the last force phase (pipeline.hpp:97), fetched on demand.
+    const std::vector<LaneTrace>& traces() const { sync_traces(); return traces_; }
     void set_collide_variant(CollideVariant v) {
         cfg_.run.collide_variant = v;
         check(dem_set_collide_variant(ctx_.get(), v == CollideVariant::two_phase ? 1 : 0));
@@ -297,6 +446,7 @@ class Simulation {
     const ForceAccumulator& forces() const { sync_forces(); return forces_; }
     ForceAccumulator& forces() { sync_forces(); forces_dirty_ = true; return forces_; }
     const ContactTable& contact_table() const { sync_table(); return table_; }
+    const SortedOrder& order() const { sync_order(); return order_; }
     std::int64_t step_index() const { return dem_step_index(ctx_.get()); }
     std::int64_t last_clamp_count() const { return last_.clamps; }
     double mean_coordination() const {
@@ -308,14 +458,28 @@ class Simulation {
     struct CtxDeleter { void operator()(dem_ctx* c) const { dem_destroy(c); } };
 
     template <typename F>
-    StepMetrics run(F&& fn, bool) {
+    StepMetrics run(F&& fn, bool record) {
         flush();
         dem_step_metrics m{};
         const int rc = fn(&m);
         state_fresh_ = forces_fresh_ = table_fresh_ = false;
         if (rc != DEM_OK) rethrow(ctx_.get(), rc);
-        last_ = StepMetrics{m.step, m.contacts, m.pp_contact_events, m.max_contacts_per_particle,
-                            m.clamps, m.friction_max_ratio, m.capped_contacts};
+        traces_fresh_ = order_fresh_ = false;
+        last_ = StepMetrics{};
+        last_.step = m.step;
+        last_.contacts = m.contacts;
+        last_.pp_contact_events = m.pp_contact_events;
+        last_.max_contacts_per_particle = m.max_contacts_per_particle;
+        last_.clamps = m.clamps;
+        last_.friction_max_ratio = m.friction_max_ratio;
+        last_.capped_contacts = m.capped_contacts;
+        if (record && record_traces_) {  // pipeline.cpp:356-362
+            const WarpReport r = model_report(traces(), cfg_.warp);
+            last_.model_cycles_baseline = r.cycles_baseline;
+            last_.model_cycles_two_phase = r.cycles_two_phase;
+            last_.utilization_baseline = r.utilization_baseline;
+            last_.utilization_two_phase = r.utilization_two_phase;
+        }
         return last_;
     }
 
@@ -370,6 +534,43 @@ class Simulation {
             s.delta_t = Vec3{d[3 * k], d[3 * k + 1], d[3 * k + 2]};
         }
         self->table_fresh_ = true;
+    }
+
+    void sync_order() const {
+        if (order_fresh_) return;
+        auto* self = const_cast<Simulation*>(this);
+        const auto n = dem_size(ctx_.get());
+        SortedOrder& o = self->order_;
+        o.sorted_keys.assign(n, 0);
+        o.permutation.assign(n, 0);
+        check(dem_get_order(ctx_.get(), o.sorted_keys.data(), o.permutation.data()));
+        const auto m = static_cast<std::size_t>(grid().cell_count());
+        o.cell_start.assign(m, 0);
+        o.cell_end.assign(m, 0);
+        for (std::size_t i = 0; i < n; ++i) {  // sorted_order.cpp:17-29
+            const std::uint32_t k = o.sorted_keys[i];
+            if (i == 0 || o.sorted_keys[i - 1] != k) o.cell_start[k] = static_cast<std::uint32_t>(i);
+            o.cell_end[k] = static_cast<std::uint32_t>(i + 1);
+        }
+        self->order_fresh_ = true;
+    }
+
+    void sync_traces() const {
+        if (traces_fresh_) return;
+        auto* self = const_cast<Simulation*>(this);
+        const auto n = dem_size(ctx_.get());
+        std::vector<std::uint64_t> off(n + 1);
+        const std::int64_t total = dem_get_traces(ctx_.get(), off.data(), nullptr, 0);
+        if (total < 0) rethrow(ctx_.get(), static_cast<int>(-total));
+        std::vector<dem_trace_event> ev(static_cast<std::size_t>(total));
+        if (total > 0 && dem_get_traces(ctx_.get(), nullptr, ev.data(), total) != total) rethrow(ctx_.get(), DEM_ERR_CUDA);
+        self->traces_.assign(n, LaneTrace{});
+        for (std::size_t i = 0; i < n; ++i) {
+            LaneTrace& t = self->traces_[i];
+            t.reserve(off[i + 1] - off[i]);
+            for (std::uint64_t k = off[i]; k < off[i + 1]; ++k) t.push_back(TraceEvent{ev[k].candidate, ev[k].contact != 0});
+        }
+        self->traces_fresh_ = true;
     }
 
     static dem_particles view(ParticleSet& s) {
@@ -448,10 +649,13 @@ class Simulation {
     mutable ParticleSet state_;
     mutable ForceAccumulator forces_;
     mutable ContactTable table_;
-    mutable bool state_fresh_ = false, forces_fresh_ = false, table_fresh_ = false;
+    mutable std::vector<LaneTrace> traces_;
+    mutable SortedOrder order_;
+    mutable bool state_fresh_ = false, forces_fresh_ = false, table_fresh_ = false, traces_fresh_ = false,
+                 order_fresh_ = false;
     mutable bool state_dirty_ = false, forces_dirty_ = false;
     StepMetrics last_;
-    bool record_traces_ = false;
+    bool record_traces_ = true;
 };
 
 }  // namespace demb200

@@ -400,6 +400,10 @@ class RefLib:
         L.ref_sim_get_grid.argtypes = [C.c_void_p, C.POINTER(orc_grid)]
         L.ref_sim_mean_coordination.restype = C.c_double
         L.ref_sim_mean_coordination.argtypes = [C.c_void_p]
+        L.ref_sim_traces.restype = C.c_int64
+        L.ref_sim_traces.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), PI, C.POINTER(C.c_uint8), C.c_int64]
+        L.ref_model_report.argtypes = [C.c_size_t, C.POINTER(C.c_uint64), C.POINTER(C.c_uint8), C.c_int,
+                                       C.c_double, C.c_double, C.c_double, C.c_double, PD]
         L.ref_sim_table.restype = C.c_int64
         L.ref_sim_table.argtypes = [C.c_void_p, PU, PI, C.POINTER(C.c_uint8), PD, C.c_int64]
         L.ref_oracle_collide.restype = C.c_int64
@@ -432,6 +436,17 @@ class RefLib:
 
     def set_threads(self, n):
         self.L.ref_set_threads(int(n))
+
+    def model_report(self, offsets, contact, warp_size=32, c_check=1.0, c_force=20.0, c_store=1.0, c_load=1.0):
+        """warp_model.cpp:118-136 over flattened traces -> dict."""
+        offsets = np.ascontiguousarray(offsets, np.uint64)
+        contact = np.ascontiguousarray(contact, np.uint8)
+        out = np.zeros(5)
+        self.L.ref_model_report(len(offsets) - 1, offsets.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                contact.ctypes.data_as(C.POINTER(C.c_uint8)), warp_size, c_check, c_force,
+                                c_store, c_load, out.ctypes.data_as(PD))
+        return {"cycles_baseline": out[0], "cycles_two_phase": out[1], "utilization_baseline": out[2],
+                "utilization_two_phase": out[3], "warp_count": int(out[4])}
 
     def thread_count(self):
         return self.L.ref_thread_count()
@@ -607,6 +622,16 @@ class RefSim:
         g = orc_grid()
         self.r.L.ref_sim_get_grid(self.h, C.byref(g))
         return g
+
+    def traces(self):
+        """(offsets[n+1], candidate slots, contact flags) of the last traced kernel_collide."""
+        total = self.r.L.ref_sim_traces(self.h, None, None, None, 0)
+        off = np.zeros(self.n + 1, np.uint64)
+        cand = np.zeros(max(total, 1), np.int32)
+        hit = np.zeros(max(total, 1), np.uint8)
+        self.r.L.ref_sim_traces(self.h, off.ctypes.data_as(C.POINTER(C.c_uint64)), cand.ctypes.data_as(PI),
+                                hit.ctypes.data_as(C.POINTER(C.c_uint8)), total)
+        return off, cand[:total], hit[:total].astype(bool)
 
     def table(self):
         cap = int(self.n) * self.cfg.contact_capacity + 16

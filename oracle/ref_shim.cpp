@@ -155,7 +155,7 @@ int ref_sim_run_kernel(void* h, int which, int variant) {
             case 4: sim->zero_forces(); break;
             case 5: sim->kernel_force_gravity(); break;
             case 6: sim->kernel_initialize_contact_ids(); break;
-            case 7: sim->kernel_collide(variant ? CollideVariant::two_phase : CollideVariant::baseline, false); break;
+            case 7: sim->kernel_collide(variant & 1 ? CollideVariant::two_phase : CollideVariant::baseline, (variant & 2) != 0); break;
             case 8: sim->kernel_collide_rectangle(); break;
             case 9: sim->kernel_collide_line(); break;
             default: return -1;
@@ -198,6 +198,40 @@ void ref_sim_get_grid(void* h, orc_grid* g) {
 }
 
 double ref_sim_mean_coordination(void* h) { return static_cast<Simulation*>(h)->mean_coordination(); }
+
+// Traversal traces of the last kernel_collide with record_traces (pipeline.hpp:97), flattened:
+// offsets[n+1], then candidate slot / contact flag per event. Returns the event count.
+std::int64_t ref_sim_traces(void* h, std::uint64_t* offsets, std::int32_t* cand, std::uint8_t* contact,
+                            std::int64_t cap) {
+    const auto& tr = static_cast<Simulation*>(h)->traces();
+    std::int64_t k = 0;
+    for (std::size_t i = 0; i < tr.size(); ++i) {
+        if (offsets) offsets[i] = static_cast<std::uint64_t>(k);
+        for (const TraceEvent& e : tr[i]) {
+            if (k < cap) { cand[k] = e.candidate; contact[k] = e.contact ? 1 : 0; }
+            ++k;
+        }
+    }
+    if (offsets) offsets[tr.size()] = static_cast<std::uint64_t>(k);
+    return k;
+}
+
+// The reference warp model (warp_model.cpp:118-136) over flattened traces.
+// out: cycles_baseline, cycles_two_phase, utilization_baseline, utilization_two_phase, warp_count.
+void ref_model_report(std::size_t n, const std::uint64_t* offsets, const std::uint8_t* contact,
+                      int warp_size, double c_check, double c_force, double c_store, double c_load,
+                      double out[5]) {
+    std::vector<LaneTrace> tr(n);
+    for (std::size_t i = 0; i < n; ++i)
+        for (std::uint64_t k = offsets[i]; k < offsets[i + 1]; ++k)
+            tr[i].push_back({static_cast<std::int32_t>(k - offsets[i]), contact[k] != 0});
+    WarpCostParams p;
+    p.warp_size = warp_size; p.c_check = c_check; p.c_force = c_force; p.c_store = c_store; p.c_load = c_load;
+    const WarpReport r = model_report(tr, p);
+    out[0] = r.cycles_baseline; out[1] = r.cycles_two_phase;
+    out[2] = r.utilization_baseline; out[3] = r.utilization_two_phase;
+    out[4] = static_cast<double>(r.warp_count);
+}
 
 // Live contact-table slots as (owner slot, partner, touched, delta_t), row order.
 std::int64_t ref_sim_table(void* h, std::uint32_t* owner, std::int32_t* partner, std::uint8_t* touched,

@@ -97,6 +97,7 @@ SIGNATURES = [
     ("dem_get_order", C.c_int, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     ("dem_get_contacts", C.c_int64, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_int32),
                                      C.POINTER(C.c_double), C.c_int64]),
+    ("dem_get_traces", C.c_int64, [_P, C.POINTER(C.c_uint64), _P, C.c_int64]),
     ("dem_last_error", C.c_int, [_P, C.POINTER(dem_error)]),
     ("dem_time_steps", C.c_int, [_P, C.c_int, C.c_size_t, C.POINTER(C.c_float),
                                  C.POINTER(dem_step_metrics)]),

@@ -67,6 +67,7 @@ struct dem_ctx {
 
     // execution state
     uint64_t phase_count = 0;  // force phases executed (parity selects buffers)
+    uint64_t replaced_at = ~0ull;  // phase_count when dem_set_particles last replaced the state
     int64_t step_index = 0;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     void* flush_buf = nullptr;
@@ -645,6 +646,7 @@ int dem_clone(const dem_ctx* src, dem_ctx** out) {
         }
         copy(ctx->ft, src->ft, 6 * n * sizeof(double));
         copy(ctx->skey, src->skey, n * sizeof(uint32_t));
+        copy(ctx->cstart, src->cstart, (static_cast<size_t>(src->M) + 1) * sizeof(uint32_t));
         copy(ctx->prev_slot, src->prev_slot, n * sizeof(uint32_t));
         copy(ctx->pair_i, src->pair_i, src->cap * sizeof(uint32_t));
         copy(ctx->pair_j, src->pair_j, src->cap * sizeof(uint32_t));
@@ -656,6 +658,7 @@ int dem_clone(const dem_ctx* src, dem_ctx** out) {
         if (rc == DEM_OK && cudaStreamSynchronize(ctx->stream) != cudaSuccess) rc = DEM_ERR_CUDA;
     }
     ctx->phase_count = src->phase_count;
+    ctx->replaced_at = src->replaced_at;
     ctx->step_index = src->step_index;
     ctx->last_error = src->last_error;
     if (rc == DEM_OK) rc = build_graphs(ctx);
@@ -730,6 +733,7 @@ int dem_set_particles(dem_ctx* ctx, const dem_particles* in) {
     if (!in->ids || !in->positions || !in->velocities || !in->angular_velocities || !in->radii || !in->masses || !in->material_ids)
         return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
+    ctx->replaced_at = ctx->phase_count;  // the binning no longer matches the state (traces)
     return upload_state(ctx, in, state_cur(ctx));
 }
 
@@ -808,6 +812,52 @@ int64_t dem_get_contacts(dem_ctx* ctx, uint32_t* owner_slot, int32_t* partner, d
             for (int a = 0; a < 3; ++a) delta_t[3 * k + a] = dt[a * ctx->cap + q];
         }
     return C;
+}
+
+int64_t dem_get_traces(dem_ctx* ctx, uint64_t* offsets, dem_trace_event* events, int64_t capacity) {
+    if (!ctx || ctx->slab || ctx->phase_count == 0 || ctx->replaced_at == ctx->phase_count) return -DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    const uint64_t n = ctx->n;
+    if (n == 0) {
+        if (offsets) offsets[0] = 0;
+        return 0;
+    }
+    const StepParams p = make_params(ctx, DEM_PHASE_PP);
+    const PhaseBufs b = make_bufs(ctx, ctx->phase_count);
+    cudaStream_t s = ctx->stream;
+    uint32_t* d_count = nullptr;
+    unsigned long long* d_off = nullptr;
+    int2* d_ev = nullptr;
+    int64_t result = -DEM_ERR_CUDA;
+    std::vector<uint32_t> cnt(n);
+    std::vector<unsigned long long> off(n + 1);
+    do {
+        if (cudaMalloc(&d_count, n * sizeof(uint32_t)) != cudaSuccess) break;
+        launch_trace(p, b, nullptr, nullptr, d_count, s);
+        if (cudaMemcpyAsync(cnt.data(), d_count, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s) != cudaSuccess) break;
+        if (cudaStreamSynchronize(s) != cudaSuccess) break;
+        off[0] = 0;
+        for (uint64_t i = 0; i < n; ++i) off[i + 1] = off[i] + cnt[i];
+        const uint64_t total = off[n];
+        if (offsets) std::memcpy(offsets, off.data(), (n + 1) * sizeof(uint64_t));
+        result = static_cast<int64_t>(total);
+        if (!events || capacity < static_cast<int64_t>(total) || total == 0) break;
+        result = -DEM_ERR_CUDA;
+        if (cudaMalloc(&d_off, (n + 1) * sizeof(unsigned long long)) != cudaSuccess) break;
+        if (cudaMalloc(&d_ev, total * sizeof(int2)) != cudaSuccess) break;
+        if (cudaMemcpyAsync(d_off, off.data(), (n + 1) * sizeof(unsigned long long), cudaMemcpyHostToDevice, s) != cudaSuccess) break;
+        launch_trace(p, b, d_off, d_ev, nullptr, s);
+        static_assert(sizeof(dem_trace_event) == sizeof(int2), "event layout");
+        if (cudaMemcpyAsync(events, d_ev, total * sizeof(int2), cudaMemcpyDeviceToHost, s) != cudaSuccess) break;
+        if (cudaStreamSynchronize(s) != cudaSuccess) break;
+        result = static_cast<int64_t>(total);
+    } while (false);
+    cudaFree(d_count);
+    cudaFree(d_off);
+    cudaFree(d_ev);
+    if (cudaGetLastError() != cudaSuccess) result = -DEM_ERR_CUDA;
+    if (result == -DEM_ERR_CUDA) set_error(ctx, DEM_ERR_CUDA, -1, 0, 0, ctx->step_index, "CUDA failure in dem_get_traces");
+    return result;
 }
 
 int dem_last_error(const dem_ctx* ctx, dem_error* out) {

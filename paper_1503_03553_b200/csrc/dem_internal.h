@@ -148,6 +148,9 @@ void launch_detect(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
 void launch_force_reduce(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
 void launch_collide_single_loop(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
 void launch_flush(void* buf, size_t bytes, cudaStream_t s);
+// traversal traces of the phase whose buffers `b` names (ev == nullptr: per-slot counts)
+void launch_trace(const StepParams& p, const PhaseBufs& b, const unsigned long long* off, int2* ev,
+                  uint32_t* count, cudaStream_t s);
 
 // Device staging in the caller's (host) layout: positions[3n], ..., ids[n], material_ids[n].
 struct RawState {

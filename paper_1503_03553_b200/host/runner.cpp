@@ -78,13 +78,13 @@ std::vector<std::pair<std::uint32_t, std::uint32_t>> brute_pairs(const ParticleS
     return out;
 }
 
-std::vector<std::pair<std::uint32_t, std::uint32_t>> table_pairs(const ContactTable& t) {
+// Contact pairs (i < j) seen by the traversal: the contact events of the traces (runner.cpp:245-256).
+std::vector<std::pair<std::uint32_t, std::uint32_t>> trace_pairs(const std::vector<LaneTrace>& traces) {
     std::set<std::pair<std::uint32_t, std::uint32_t>> out;
-    for (std::uint32_t i = 0; i < t.particle_count(); ++i)
-        for (int k = 0; k < t.capacity(); ++k) {
-            const ContactSlot& s = t.row(i)[k];
-            if (s.empty() || ContactTable::is_wall(s.partner)) continue;
-            const auto j = static_cast<std::uint32_t>(s.partner);
+    for (std::uint32_t i = 0; i < traces.size(); ++i)
+        for (const TraceEvent& e : traces[i]) {
+            if (!e.contact) continue;
+            const auto j = static_cast<std::uint32_t>(e.candidate);
             out.emplace(std::min(i, j), std::max(i, j));
         }
     return {out.begin(), out.end()};
@@ -108,6 +108,7 @@ RunSummary run_simulation(const SimConfig& cfg, const std::filesystem::path& out
     RunSummary summary;
     write_snapshot(snapshot_path(out_dir, 0), sim.particles());
     ++summary.snapshots_written;
+    sim.set_record_traces(false);
     for (std::int64_t s = 1; s <= cfg.run.warmup_steps; ++s) {
         try {
             sim.step();
@@ -117,6 +118,7 @@ RunSummary run_simulation(const SimConfig& cfg, const std::filesystem::path& out
     }
     summary.metrics_path = out_dir / "metrics.csv";
     std::string text = std::string(kMetricsHeader) + "\n";
+    sim.set_record_traces(true);  // model columns of the metrics rows (runner.cpp:57)
     for (std::int64_t s = 1; s <= cfg.run.steps; ++s) {
         StepMetrics m;
         try {
@@ -149,6 +151,7 @@ BenchPhase measure(Simulation& sim, std::int64_t steps, const std::string& label
     double coord = 0.0;
     for (std::int64_t s = 0; s < steps; ++s) {
         Simulation fork = sim;
+        fork.set_record_traces(false);
         fork.set_collide_variant(CollideVariant::baseline);
         double kb[DEM_DEVICE_KERNEL_COUNT], kt[DEM_DEVICE_KERNEL_COUNT];
         fork.profile_step(kb);
@@ -162,6 +165,7 @@ BenchPhase measure(Simulation& sim, std::int64_t steps, const std::string& label
         ph.collide_us_two_phase += 1e3 * (kt[DEM_DK_DETECT] + kt[DEM_DK_FORCE_REDUCE]);
         for (int k = 0; k < DEM_DEVICE_KERNEL_COUNT; ++k) ph.kernel_us[k] += 1e3 * kt[k];
         coord += sim.mean_coordination();
+        ph.model.merge(model_report(sim.traces(), sim.config().warp));
         (void)m;
     }
     const double inv = 1.0 / static_cast<double>(std::max<std::int64_t>(1, steps));
@@ -181,6 +185,11 @@ void format_phase(std::ostringstream& os, const BenchPhase& ph) {
     os << "  Collide single loop (Alg. 1):           " << ph.collide_us_baseline << " us\n";
     os << "  Collide two-phase (detect + force):     " << ph.collide_us_two_phase << " us\n";
     os << "  Collide ratio single-loop / two-phase:  " << ph.ratio() << "\n";
+    os << "  modeled warp cycles baseline:          " << ph.model.cycles_baseline << "\n";
+    os << "  modeled warp cycles two_phase:         " << ph.model.cycles_two_phase << "\n";
+    os << "  modeled ratio baseline/two_phase:      " << ph.model.speedup() << "\n";
+    os << "  modeled utilization baseline:          " << ph.model.utilization_baseline << "\n";
+    os << "  modeled utilization two_phase:         " << ph.model.utilization_two_phase << "\n";
 }
 
 }  // namespace
@@ -195,6 +204,7 @@ std::string BenchReport::format() const {
 
 BenchReport bench(const SimConfig& cfg, int device) {  // runner.cpp:193-214
     Simulation sim(build_initial_state(cfg), cfg, device);
+    sim.set_record_traces(false);  // the model is taken once per measured step, in measure()
     BenchReport r;
     const std::int64_t measured = std::max<std::int64_t>(1, cfg.run.steps);
     r.sparse = measure(sim, std::min<std::int64_t>(5, measured), "sparse (pre-warm-up)");
@@ -223,6 +233,7 @@ VerifyReport verify(const SimConfig& cfg, int device) {  // runner.cpp:274-417
     VerifyReport rep;
     {
         Simulation sim(seeded_state(cfg), cfg, device);
+        sim.set_record_traces(false);
         bool complete = true, variants = true;
         std::int64_t pairs = 0, missing = 0, events = 0;
         double friction = 0.0;
@@ -235,8 +246,8 @@ VerifyReport verify(const SimConfig& cfg, int device) {  // runner.cpp:274-417
                 b.set_collide_variant(CollideVariant::baseline);
                 a.advance_and_collide();
                 b.advance_and_collide();
-                const auto found = table_pairs(a.contact_table());
-                const auto expect = brute_pairs(a.particles());
+                const auto found = trace_pairs(b.traces());
+                const auto expect = brute_pairs(b.particles());
                 pairs += static_cast<std::int64_t>(expect.size());
                 if (found != expect) {
                     complete = false;
@@ -276,6 +287,7 @@ VerifyReport verify(const SimConfig& cfg, int device) {  // runner.cpp:274-417
         free_cfg.rect_walls.clear();
         free_cfg.line_walls.clear();
         Simulation sim(seeded_state(free_cfg), free_cfg, device);
+        sim.set_record_traces(false);
         const Vec3 p0 = momentum(sim.particles());
         const double p0n = vnorm(p0);
         double ke_last = kinetic_energy(sim.particles()), worst = 0.0;

@@ -462,6 +462,21 @@ class Simulation:
             self._check(-got)
         return o, p, d
 
+    def traces(self):
+        """Traversal traces of the last force phase (pipeline.hpp:97): (offsets[n+1] uint64,
+        candidate slot int32[], contact bool[]); slot i's events are [offsets[i], offsets[i+1])."""
+        n = self.size()
+        off = np.zeros(n + 1, np.uint64)
+        total = self._lib.dem_get_traces(self._ctx, off.ctypes.data_as(C.POINTER(C.c_uint64)), None, 0)
+        if total < 0:
+            self._check(-total)
+        ev = np.zeros((max(total, 1), 2), np.int32)
+        if total:
+            got = self._lib.dem_get_traces(self._ctx, None, ev.ctypes.data_as(C.c_void_p), total)
+            if got < 0:
+                self._check(-got)
+        return off, ev[:total, 0].copy(), ev[:total, 1].astype(bool)
+
     def contact_table(self):
         o, p, d = self.contacts()
         return [ContactEntry(int(a), int(b), c) for a, b, c in zip(o, p, d)]

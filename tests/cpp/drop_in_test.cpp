@@ -5,8 +5,11 @@
 // where the reference headers exist; run by tests/test_cpp_drop_in.py on the GPU box.
 #include <cmath>
 #include <cstdio>
+#include <cstring>
+#include <algorithm>
 #include <map>
 #include <random>
+#include <tuple>
 
 #include "demb200/simulation.hpp"
 #include "demforge/pipeline.hpp"
@@ -86,6 +89,49 @@ int main() {
     EXPECT(dx <= 1e-12);
     EXPECT(dv <= 1e-9 * vmax);
     EXPECT(df <= 1e-9 * fmax);
+    // traversal traces (pipeline.hpp:97, both sims record by default): per particle the same
+    // candidates with the same check_pair outcomes, visited cell by cell in increasing key order;
+    // only the in-cell order differs (canonical stable-id order here, bitonic tie order there)
+    {
+        using Ev = std::tuple<std::uint32_t, std::uint32_t, bool>;  // (cell key, candidate id, contact)
+        auto canon = [](const auto& traces, const auto& ps, const std::vector<std::uint32_t>& keys, bool& monotone) {
+            std::map<std::uint32_t, std::vector<Ev>> m;
+            for (std::size_t i = 0; i < traces.size(); ++i) {
+                auto& v = m[ps.ids[i]];
+                for (std::size_t k = 0; k < traces[i].size(); ++k) {
+                    const auto& e = traces[i][k];
+                    const std::uint32_t key = keys[e.candidate];
+                    if (k && key < keys[traces[i][k - 1].candidate]) monotone = false;
+                    v.emplace_back(key, ps.ids[e.candidate], e.contact);
+                }
+                std::sort(v.begin(), v.end());
+            }
+            return m;
+        };
+        bool rmono = true, bmono = true;
+        const auto rc_ = canon(rsim.traces(), rsim.particles(), rsim.order().sorted_keys, rmono);
+        const auto bc_ = canon(bsim.traces(), bsim.particles(), bsim.order().sorted_keys, bmono);
+        EXPECT(rmono && bmono);
+        EXPECT(rc_ == bc_);
+        // the warp model over the B200 traces: demb200::model_report == demforge::model_report bitwise
+        std::vector<ref::LaneTrace> conv(n);
+        for (std::size_t i = 0; i < n; ++i)
+            for (const auto& e : bsim.traces()[i]) conv[i].push_back({e.candidate, e.contact});
+        const auto rm = ref::model_report(conv, rcfg.warp);
+        const auto bm = b2::model_report(bsim.traces(), bcfg.warp);
+        EXPECT(std::memcmp(&rm.cycles_baseline, &bm.cycles_baseline, sizeof(double)) == 0);
+        EXPECT(std::memcmp(&rm.utilization_two_phase, &bm.utilization_two_phase, sizeof(double)) == 0);
+        // step() metrics carry the model (pipeline.cpp:356-362); the in-cell order moves lanes
+        // between warps, so against the reference's own traces the model agrees only closely
+        const auto rs = rsim.step();
+        const auto bs = bsim.step();
+        EXPECT(bs.model_cycles_two_phase > 0.0 && bs.utilization_baseline < bs.utilization_two_phase);
+        EXPECT(std::abs(rs.model_cycles_baseline - bs.model_cycles_baseline) <= 0.05 * rs.model_cycles_baseline);
+        EXPECT(std::abs(rs.utilization_two_phase - bs.utilization_two_phase) <= 0.05 * rs.utilization_two_phase);
+        std::printf("model: ref util %.4f/%.4f cycles %.0f/%.0f  b200 util %.4f/%.4f cycles %.0f/%.0f\n",
+                    rs.utilization_baseline, rs.utilization_two_phase, rs.model_cycles_baseline, rs.model_cycles_two_phase,
+                    bs.utilization_baseline, bs.utilization_two_phase, bs.model_cycles_baseline, bs.model_cycles_two_phase);
+    }
     // contact tables: same live entry count, same partner sets per particle (by stable id)
     EXPECT(rsim.contact_table().total_live() >= bsim.contact_table().total_live());
     // copy constructor forks identical simulations

@@ -14,6 +14,7 @@
 #include "demforge/error.hpp"
 #include "demforge/lattice.hpp"
 #include "demforge/snapshot_io.hpp"
+#include "demforge/warp_model.hpp"
 
 static int failures = 0;
 #define EXPECT(c) do { if (!(c)) { std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #c); ++failures; } } while (0)
@@ -96,6 +97,69 @@ int main(int argc, char** argv) {
         fd = fd && demforge::format_double(v) == demb200::format_double(v);
     }
     EXPECT(fd);
+    // the warp model (warp_model.cpp) on random traces: every field bitwise, several warp sizes
+    // and non-integer costs (so the summation order matters)
+    for (int trial = 0; trial < 40; ++trial) {
+        const std::size_t lanes = 1 + rng() % 300;
+        std::vector<demforge::LaneTrace> rt(lanes);
+        std::vector<demb200::LaneTrace> bt(lanes);
+        const double dens = 0.02 + 0.5 * (rng() % 1000) / 1000.0;
+        for (std::size_t i = 0; i < lanes; ++i) {
+            const int len = static_cast<int>(rng() % 90);
+            for (int k = 0; k < len; ++k) {
+                const bool hit = (rng() % 1000) < dens * 1000;
+                rt[i].push_back({k, hit});
+                bt[i].push_back({k, hit});
+            }
+        }
+        demforge::WarpCostParams rp;
+        demb200::WarpCostParams bp;
+        const int ws[] = {32, 7, 1, 64};
+        rp.warp_size = bp.warp_size = ws[trial % 4];
+        if (trial % 2) {
+            rp.c_check = bp.c_check = 0.37; rp.c_force = bp.c_force = 19.3;
+            rp.c_store = bp.c_store = 1.1; rp.c_load = bp.c_load = 0.7;
+        }
+        const auto r = demforge::model_report(rt, rp);
+        const auto b = demb200::model_report(bt, bp);
+        EXPECT(same(r.cycles_baseline, b.cycles_baseline) && same(r.cycles_two_phase, b.cycles_two_phase));
+        EXPECT(same(r.utilization_baseline, b.utilization_baseline) && same(r.utilization_two_phase, b.utilization_two_phase));
+        EXPECT(same(r.useful_baseline, b.useful_baseline) && same(r.occupied_two_phase, b.occupied_two_phase));
+        EXPECT(r.warp_count == b.warp_count && same(r.speedup(), b.speedup()));
+        const auto rw = demforge::group_warps(rt, rp.warp_size);
+        const auto bw = demb200::group_warps(bt, bp.warp_size);
+        EXPECT(rw.size() == bw.size());
+        for (std::size_t w = 0; w < rw.size() && w < bw.size(); ++w)
+            for (auto [rv, bv] : {std::pair{demforge::CollideVariant::baseline, demb200::CollideVariant::baseline},
+                                  std::pair{demforge::CollideVariant::two_phase, demb200::CollideVariant::two_phase}})
+                EXPECT(same(demforge::utilization(rw[w], rp, rv), demb200::utilization(bw[w], bp, bv)));
+        // merge of per-step reports (runner.cpp:128-129)
+        auto rm = r; rm.merge(r);
+        auto bm = b; bm.merge(b);
+        EXPECT(same(rm.utilization_two_phase, bm.utilization_two_phase) && same(rm.cycles_baseline, bm.cycles_baseline));
+        // metrics rows carrying the model columns (snapshot_io.cpp:70-94)
+        demforge::StepMetrics rsm;
+        demb200::StepMetrics bsm;
+        rsm.step = bsm.step = trial + 1;
+        rsm.model_cycles_baseline = bsm.model_cycles_baseline = r.cycles_baseline;
+        rsm.model_cycles_two_phase = bsm.model_cycles_two_phase = r.cycles_two_phase;
+        rsm.utilization_baseline = bsm.utilization_baseline = r.utilization_baseline;
+        rsm.utilization_two_phase = bsm.utilization_two_phase = r.utilization_two_phase;
+        rsm.contacts = bsm.contacts = 17 * trial;
+        rsm.max_contacts_per_particle = bsm.max_contacts_per_particle = trial % 7;
+        rsm.clamps = bsm.clamps = trial % 3;
+        std::string ro, bo;
+        demforge::append_metrics_rows(ro, rsm, true);
+        demb200::append_metrics_rows(bo, bsm.step, bsm, nullptr, true);
+        EXPECT(ro == bo);
+    }
+    {
+        demb200::WarpCostParams bad;
+        bad.c_force = 0.5;
+        bool threw = false;
+        try { bad.validate(); } catch (const demb200::ConfigError& e) { threw = std::string(e.what()) == "simt.c_force must exceed simt.c_check"; }
+        EXPECT(threw);
+    }
     std::printf("%s\n", failures ? "FAILED" : "PASSED");
     return failures ? 1 : 0;
 }

@@ -4,8 +4,10 @@ run / bench / verify CLI, against the reference.
 CPU: tests/cpp/host_test runs the reference's parse_config_text / build_initial_state /
 write_snapshot side by side with demb200's (same values, same bytes, same error messages).
 GPU: `dem_b200 run` reproduces the reference CLI's `run` outputs (tests/golden/run_*, written by
-the reference's run_simulation): snapshots byte-identical, metrics rows identical except the
-analytic-SIMT-model columns the B200 path does not produce."""
+the reference's run_simulation): snapshots and metrics.csv byte-identical, including the
+warp-model columns computed from the B200 traversal traces (in general those agree only closely,
+because the in-cell order differs from the reference's bitonic tie order and moves lanes between
+warps; on these two configurations they agree exactly)."""
 import csv
 import os
 import subprocess
@@ -58,7 +60,17 @@ def test_cli_run_matches_reference_outputs(cuda, name):
         assert sorted(f for f in os.listdir(d) if f.startswith("snapshot_")) == snaps
         for f in snaps:
             assert open(os.path.join(d, f), "rb").read() == open(os.path.join(gold, f), "rb").read(), f
-        assert _metrics(os.path.join(d, "metrics.csv")) == _metrics(os.path.join(gold, "metrics.csv"))
+        got, want = os.path.join(d, "metrics.csv"), os.path.join(gold, "metrics.csv")
+        assert _metrics(got) == _metrics(want)
+        g_rows, w_rows = _metrics(got, False)[1:], _metrics(want, False)[1:]
+        exact = 0
+        for g, w in zip(g_rows, w_rows):
+            gv, wv = [float(x) for x in g[3:7]], [float(x) for x in w[3:7]]
+            exact += gv == wv
+            for a, b in zip(gv, wv):
+                assert abs(a - b) <= 0.05 * abs(b) + 1e-12, (g, w)
+        print(f"{name}: warp-model columns exact in {exact}/{len(w_rows)} rows")
+        assert open(got, "rb").read() == open(want, "rb").read()
 
 
 @pytest.mark.gpu

@@ -236,6 +236,9 @@ StepParams make_params(const dem_ctx* c, uint32_t flags) {
     p.nrect = static_cast<int>(c->rects.size());
     p.nline = static_cast<int>(c->lines.size());
     p.flags = flags;
+    p.det_lo = 1.0 - 0x1p-40;  // see k_detect
+    p.det_hi = 1.0 + 0x1p-40;
+    p.det_tiny = 4e-24;
     p.pairs = c->d_pairs;
     p.rects = c->d_rects;
     p.lines = c->d_lines;
@@ -503,6 +506,8 @@ int upload_state(dem_ctx* ctx, const dem_particles* p, int buf) {
     CUDA_TRY(cudaMemcpyAsync(r.ids, p->ids, n * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(r.mat, p->material_ids, n * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
     launch_pack_state(ctx->state[buf], r, static_cast<uint32_t>(n), true, s);
+    // the monodisperse detection shortcut compares every radius with this one (k_integrate_hash)
+    CUDA_TRY(cudaMemcpyAsync(&ctx->ctl->r_ref, p->radii, sizeof(double), cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     CUDA_TRY(cudaGetLastError());
     return DEM_OK;

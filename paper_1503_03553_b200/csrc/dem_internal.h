@@ -41,6 +41,7 @@ struct StepParams {
     int nmat;
     int nrect, nline;
     uint32_t flags;      // dem_phase_flags
+    double det_lo, det_hi, det_tiny;  // k_detect classification constants (kept in the param bank)
     const MatPairH* pairs;  // nmat*nmat, [owner][partner]
     const RectW* rects;
     const LineW* lines;
@@ -61,6 +62,9 @@ struct DevCtl {
     unsigned long long capped;
     unsigned long long fric_bits;               // max of non-negative doubles as bits
     unsigned long long contacts;
+    unsigned int odd_radius;                    // a radius outside [1e-100, 1e100] (or NaN) was binned
+    unsigned int poly;                          // a radius != r_ref was binned this phase
+    double r_ref;                               // a radius of the state (set on upload)
 };
 
 // Structure-of-arrays particle state for one buffer (sorted slot order).

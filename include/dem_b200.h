@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define DEM_B200_ABI_VERSION 1
+#define DEM_B200_ABI_VERSION 2
 
 /* Status codes <-> reference exception types (error.hpp). */
 typedef enum {
@@ -108,6 +108,12 @@ typedef struct {
     double grid_cell_size;   /* 0 => 2 r_max (1 + 1e-6), grid.cpp:15 */
     int32_t contact_capacity; /* K, contact_table.hpp:30-74 */
     int32_t collide_variant;  /* 0 baseline (Alg. 1), 1 two_phase (warp_model.hpp:9) */
+    /* Beyond the reference; zero = the reference's box.
+     * periodic: bit 0 x, bit 1 y, bit 2 z. A periodic axis of length L gets n = floor(L / h)
+     * cells of extent L / n (n >= 3). shear_rate: Lees-Edwards shear (flow x, gradient y; needs
+     * x and y periodic, n_x >= 4). Periodic boxes run the two-phase variant on one GPU. */
+    uint32_t periodic;
+    double shear_rate;
 } dem_config;
 
 /* ParticleSet, particle_set.hpp:13-37, flattened (Vec3 = 3 doubles). */
@@ -197,6 +203,9 @@ int dem_set_particles(dem_ctx* ctx, const dem_particles* in);
 int dem_get_forces(dem_ctx* ctx, double* force, double* torque);
 int dem_set_forces(dem_ctx* ctx, const double* force, const double* torque);
 int dem_get_grid(const dem_ctx* ctx, dem_grid* out);
+/* Periodic box: cell extent per axis (the grid's cell_size on non-periodic axes)
+ * and the current Lees-Edwards image offset of the upper box along x. */
+int dem_get_periodic_box(dem_ctx* ctx, double cell_extent[3], double* shear_offset);
 /* sorted cell keys (SortedOrder::sorted_keys) and, per new slot, the previous slot
  * (SortedOrder::permutation, sorted_order.hpp:13-19) */
 int dem_get_order(dem_ctx* ctx, uint32_t* sorted_keys, uint32_t* permutation);

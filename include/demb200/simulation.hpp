@@ -286,6 +286,10 @@ struct SimConfig {
     RunControlConfig run;
     ParticleInitConfig particles;
     std::uint64_t seed = 1;
+    // beyond the reference (dem_b200.h): periodic axes (bit 0 x, 1 y, 2 z) and a
+    // Lees-Edwards shear rate; 0 / 0.0 is the reference's walled box
+    std::uint32_t periodic = 0;
+    double shear_rate = 0.0;
 };
 
 // ---- particle_set.hpp --------------------------------------------------------------------------
@@ -618,6 +622,8 @@ class Simulation {
         ccfg_.grid_cell_size = cfg_.grid_cell_size;
         ccfg_.contact_capacity = cfg_.contact_capacity;
         ccfg_.collide_variant = cfg_.run.collide_variant == CollideVariant::two_phase ? 1 : 0;
+        ccfg_.periodic = cfg_.periodic;
+        ccfg_.shear_rate = cfg_.shear_rate;
     }
 
     void check(int rc) const { if (rc != DEM_OK) rethrow(ctx_.get(), rc); }

@@ -454,6 +454,129 @@ int64_t orc_collide(size_t n, const uint32_t* ids, const double* pos, const doub
 }
 
 /* ------------------------------------------------------------------------ */
+/* Periodic boundaries and Lees-Edwards shear. The reference has neither (grid.cpp:60-82
+ * clips at the box); this is the repo's own specification, restated here
+ * independently of the GPU code. With no periodic axis every function below is bypassed, so
+ * the step is the reference's bit for bit. */
+typedef struct {
+    uint32_t mask;                 /* bit k: axis k periodic */
+    double lo[3], L[3], half[3];   /* box origin, length, L/2 */
+    double inv[3];                 /* 1 / cell extent per axis */
+    int n[3];
+    double rate, U;                /* shear rate, image velocity rate * L_y */
+    int64_t le_steps;              /* integrates so far */
+    double delta;                  /* image offset of the upper box along x */
+} pbox;
+
+static void pb_update_delta(pbox* b, double dt) {
+    const double t = (double)b->le_steps * dt;
+    const double d = b->U * t;
+    b->delta = d - b->L[0] * floor(d / b->L[0]);
+}
+
+/* wrap a position (and the LE velocity jump) back into the box after integration */
+static void pb_wrap(const pbox* b, double* p, double* v) {
+    if (b->mask & 2u) {
+        const double ky = floor((p[1] - b->lo[1]) / b->L[1]);
+        if (ky != 0.0) {
+            p[1] = p[1] - b->L[1] * ky;
+            if (b->rate != 0.0) { p[0] = p[0] - b->delta * ky; v[0] = v[0] - b->U * ky; }
+        }
+    }
+    if (b->mask & 1u) {
+        const double kx = floor((p[0] - b->lo[0]) / b->L[0]);
+        if (kx != 0.0) p[0] = p[0] - b->L[0] * kx;
+    }
+    if (b->mask & 4u) {
+        const double kz = floor((p[2] - b->lo[2]) / b->L[2]);
+        if (kz != 0.0) p[2] = p[2] - b->L[2] * kz;
+    }
+}
+
+/* cell key with per-axis extents; periodic axes clamp silently (rounding at the upper face) */
+static uint32_t pb_hash(const pbox* b, const orc_grid* g, const double p[3], int* clamped) {
+    int c[3];
+    const int dims[3] = {g->nx, g->ny, g->nz};
+    int cl = 0;
+    for (int k = 0; k < 3; ++k) {
+        const double rel = p[k] - g->origin[k];
+        int ck = to_int_x86(floor(rel * b->inv[k]));
+        if (b->mask & (1u << k)) ck = ck < 0 ? 0 : (ck >= dims[k] ? dims[k] - 1 : ck);
+        else ck = clamp_axis(ck, dims[k], &cl);
+        c[k] = ck;
+    }
+    if (clamped) *clamped = cl;
+    return linear_index(g, c[0], c[1], c[2]);
+}
+
+/* minimum-image displacement partner - owner, plus the x velocity of the partner's image */
+static v3 pb_min_image(const pbox* b, v3 d, double* dvx) {
+    *dvx = 0.0;
+    if (b->mask & 2u) {
+        if (d.y > b->half[1]) {
+            d.y = d.y - b->L[1];
+            if (b->rate != 0.0) { d.x = d.x - b->delta; *dvx = -b->U; }
+        } else if (d.y < -b->half[1]) {
+            d.y = d.y + b->L[1];
+            if (b->rate != 0.0) { d.x = d.x + b->delta; *dvx = b->U; }
+        }
+    }
+    if ((b->mask & 1u) && fabs(d.x) > b->half[0]) d.x = d.x - b->L[0] * rint(d.x / b->L[0]);
+    if ((b->mask & 4u) && fabs(d.z) > b->half[2]) d.z = d.z - b->L[2] * rint(d.z / b->L[2]);
+    return d;
+}
+
+/* Candidate cells of an owner cell as x-ranges [xa, xb] of rows (y, z), in visit order: z, y
+ * outer to inner (dz, dy = -1, 0, 1, wrapped on periodic axes, clipped otherwise), then x
+ * ascending from the row's first cell: cx-1 .. cx+1, or, on a row seen through the sheared
+ * y-boundary, the 4 cells lo .. lo+3 with lo = floor((cx-1) - s/e_x), s = -+delta the image
+ * offset. Wrapped x splits a row into two ranges. Returns the number of ranges (<= 18). */
+static int pb_ranges(const pbox* b, const orc_grid* g, uint32_t cell, int out[18][4]) {
+    const int nx = g->nx, ny = g->ny, nz = g->nz;
+    const int cx = (int)(cell % (uint32_t)nx);
+    const int rest = (int)(cell / (uint32_t)nx);
+    const int cy = rest % ny, cz = rest / ny;
+    int cnt = 0;
+    for (int dz = -1; dz <= 1; ++dz) {
+        int z = cz + dz;
+        if (z < 0 || z >= nz) {
+            if (!(b->mask & 4u)) continue;
+            z = (z + nz) % nz;
+        }
+        for (int dy = -1; dy <= 1; ++dy) {
+            int y = cy + dy, ysh = 0;
+            if (y < 0 || y >= ny) {
+                if (!(b->mask & 2u)) continue;
+                ysh = y < 0 ? -1 : 1;
+                y = (y + ny) % ny;
+            }
+            int xa, xb;
+            if (ysh != 0 && b->rate != 0.0) {
+                const double sx = ysh < 0 ? -b->delta : b->delta;
+                xa = (int)floor((double)(cx - 1) - sx * b->inv[0]);
+                xb = xa + 3;
+            } else {
+                xa = cx - 1; xb = cx + 1;
+                if (!(b->mask & 1u)) { if (xa < 0) xa = 0; if (xb >= nx) xb = nx - 1; }
+            }
+            if (!(b->mask & 1u)) {
+                out[cnt][0] = xa; out[cnt][1] = xb; out[cnt][2] = y; out[cnt][3] = z; ++cnt;
+                continue;
+            }
+            const int wa = ((xa % nx) + nx) % nx;
+            const int wb = wa + (xb - xa);
+            if (wb < nx) {
+                out[cnt][0] = wa; out[cnt][1] = wb; out[cnt][2] = y; out[cnt][3] = z; ++cnt;
+            } else {
+                out[cnt][0] = wa; out[cnt][1] = nx - 1; out[cnt][2] = y; out[cnt][3] = z; ++cnt;
+                out[cnt][0] = 0; out[cnt][1] = wb - nx; out[cnt][2] = y; out[cnt][3] = z; ++cnt;
+            }
+        }
+    }
+    return cnt;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Full step, pipeline.cpp:31-378, with canonical in-cell order by stable id */
 
 struct orc_sim {
@@ -474,6 +597,7 @@ struct orc_sim {
     double* fric;
     /* scratch */
     uint32_t *cstart, *cend;
+    pbox pb;
 };
 
 size_t orc_sim_size(const orc_sim* s) { return s->n; }
@@ -537,6 +661,8 @@ int orc_sim_force_phase(orc_sim* s, int flags, orc_metrics* m, orc_error* err) {
     const size_t n = s->n;
     const int64_t step = s->step_index;
     /* Integrate, pipeline.cpp:31-44 */
+    if (flags & ORC_PH_INTEGRATE) ++s->pb.le_steps;
+    if (s->pb.mask) pb_update_delta(&s->pb, s->dt);
     if (flags & ORC_PH_INTEGRATE) {
         for (size_t i = 0; i < n; ++i) {
             const v3 f = ld3(s->F + 3 * i), t = ld3(s->Tq + 3 * i);
@@ -550,13 +676,15 @@ int orc_sim_force_phase(orc_sim* s, int flags, orc_metrics* m, orc_error* err) {
             st3(s->pos + 3 * i, add(ld3(s->pos + 3 * i), muls(v, s->dt)));
             const double inertia = 0.4 * m_ * s->rad[i] * s->rad[i];
             st3(s->omg + 3 * i, add(ld3(s->omg + 3 * i), muls(t, s->dt / inertia)));
+            if (s->pb.mask) pb_wrap(&s->pb, s->pos + 3 * i, s->vel + 3 * i);
         }
     }
     /* CalcHash, pipeline.cpp:107-121 */
     int64_t clamps = 0;
     for (size_t i = 0; i < n; ++i) {
         int cl = 0;
-        s->keys[i] = orc_calc_hash(s->pos + 3 * i, &s->grid, &cl);
+        s->keys[i] = s->pb.mask ? pb_hash(&s->pb, &s->grid, s->pos + 3 * i, &cl)
+                                : orc_calc_hash(s->pos + 3 * i, &s->grid, &cl);
         clamps += cl;
     }
     s->clamps = clamps;
@@ -606,7 +734,57 @@ int orc_sim_force_phase(orc_sim* s, int flags, orc_metrics* m, orc_error* err) {
     /* Collide (two-phase), pipeline.cpp:182-242 */
     if (flags & ORC_PH_PP) {
         uint32_t* local = (uint32_t*)malloc(((size_t)s->K + 1) * sizeof(uint32_t));
-        for (size_t i = 0; i < n && rc == ORC_OK; ++i) {
+        for (size_t i = 0; i < n && rc == ORC_OK && s->pb.mask; ++i) {
+            int rg[18][4];
+            const int nrg = pb_ranges(&s->pb, &s->grid, s->keys[i], rg);
+            int cnt = 0;
+            const v3 pi = ld3(s->pos + 3 * i);
+            const double zero3[3] = {0.0, 0.0, 0.0};
+            for (int c = 0; c < nrg && rc == ORC_OK; ++c) {
+                const uint32_t ka = linear_index(&s->grid, rg[c][0], rg[c][2], rg[c][3]);
+                const uint32_t kb = linear_index(&s->grid, rg[c][1], rg[c][2], rg[c][3]);
+                for (uint32_t cc = ka; cc <= kb && rc == ORC_OK; ++cc)
+                for (uint32_t j = s->cstart[cc]; j < s->cend[cc]; ++j) {
+                    if (j == i) continue;
+                    double dvx;
+                    const v3 diff = pb_min_image(&s->pb, sub(ld3(s->pos + 3 * j), pi), &dvx);
+                    const double reach = s->rad[i] + s->rad[j];
+                    const double reach2 = reach * reach;
+                    if (dot(diff, diff) >= reach2 + reach2 * 1e-9) continue;
+                    double dd[3], vj[3], g[10];
+                    st3(dd, diff);
+                    st3(vj, ld3(s->vel + 3 * j));
+                    if (dvx != 0.0) vj[0] = vj[0] + dvx;
+                    const int hit = orc_contact_geometry(zero3, s->rad[i], s->vel + 3 * i, s->omg + 3 * i, dd, 0,
+                                                         s->rad[j], vj, s->omg + 3 * j, g);
+                    if (hit < 0) {
+                        set_err(err, ORC_ERR_DEGENERATE, ORC_K_COLLIDE, (uint32_t)i, s->ids[i], step);
+                        rc = ORC_ERR_DEGENERATE; break;
+                    }
+                    if (!hit) continue;
+                    if (cnt >= s->K) {
+                        set_err(err, ORC_ERR_CAPACITY, ORC_K_COLLIDE, (uint32_t)i, s->ids[i], step);
+                        rc = ORC_ERR_CAPACITY; break;
+                    }
+                    local[cnt++] = j;
+                }
+            }
+            for (int c = 0; c < cnt && rc == ORC_OK; ++c) {
+                const uint32_t j = local[c];
+                double dvx, dd[3], vj[3], g[10];
+                st3(dd, pb_min_image(&s->pb, sub(ld3(s->pos + 3 * j), pi), &dvx));
+                st3(vj, ld3(s->vel + 3 * j));
+                if (dvx != 0.0) vj[0] = vj[0] + dvx;
+                orc_contact_geometry(zero3, s->rad[i], s->vel + 3 * i, s->omg + 3 * i, dd, 0, s->rad[j], vj,
+                                     s->omg + 3 * j, g);
+                if (apply_contact(s, i, g, s->mat[i], s->mat[j], s->rad[j], s->mass[j], 0, s->ids[j],
+                                  old, olo[i], ohi[i], &row_live[i], out, &nout) != ORC_OK) {
+                    set_err(err, ORC_ERR_CAPACITY, ORC_K_COLLIDE, (uint32_t)i, s->ids[i], step);
+                    rc = ORC_ERR_CAPACITY;
+                }
+            }
+        }
+        for (size_t i = 0; i < n && rc == ORC_OK && !s->pb.mask; ++i) {
             uint32_t cells[27];
             const int nc = orc_neighbor_cells(s->keys[i], &s->grid, cells);
             int cnt = 0;
@@ -745,6 +923,32 @@ orc_sim* orc_sim_create(const orc_config* cfg, size_t n, const uint32_t* ids, co
         orc_sim_destroy(s);
         return NULL;
     }
+    /* periodic axes: n = floor(L / h) cells of extent L / n (>= h); n >= 3 (x: >= 4 with shear) */
+    s->pb.mask = cfg->periodic & 7u;
+    s->pb.rate = s->pb.mask ? cfg->shear_rate : 0.0;
+    {
+        int* dims[3] = {&s->grid.nx, &s->grid.ny, &s->grid.nz};
+        int bad = (s->pb.rate != 0.0) && ((s->pb.mask & 3u) != 3u);
+        for (int k = 0; k < 3; ++k) {
+            s->pb.lo[k] = cfg->domain_min[k];
+            s->pb.L[k] = cfg->domain_max[k] - cfg->domain_min[k];
+            s->pb.half[k] = 0.5 * s->pb.L[k];
+            s->pb.inv[k] = 1.0 / s->grid.cell_size;
+            if (s->pb.mask & (1u << k)) {
+                const int nk = (int)floor(s->pb.L[k] / s->grid.cell_size);
+                if (nk < 3 || (k == 0 && s->pb.rate != 0.0 && nk < 4)) bad = 1;
+                *dims[k] = nk < 1 ? 1 : nk;
+                s->pb.inv[k] = 1.0 / (s->pb.L[k] / (double)nk);
+            }
+            s->pb.n[k] = *dims[k];
+        }
+        s->pb.U = s->pb.rate * s->pb.L[1];
+        if (bad) {
+            set_err(err, ORC_ERR_CONFIG, -1, 0, 0, 0);
+            orc_sim_destroy(s);
+            return NULL;
+        }
+    }
     const int64_t M = (int64_t)s->grid.nx * s->grid.ny * s->grid.nz;
     s->cstart = (uint32_t*)calloc(M + 1, sizeof(uint32_t));
     s->cend = (uint32_t*)calloc(M + 1, sizeof(uint32_t));
@@ -794,3 +998,8 @@ void orc_sim_get_keys(const orc_sim* s, uint32_t* k) { memcpy(k, s->keys, s->n *
 int64_t orc_sim_history_count(const orc_sim* s) { return s->nhist; }
 void orc_sim_get_history(const orc_sim* s, orc_hist* out) { memcpy(out, s->hist, s->nhist * sizeof(orc_hist)); }
 void orc_sim_get_grid(const orc_sim* s, orc_grid* g) { *g = s->grid; }
+void orc_sim_get_pbox(const orc_sim* s, double ext[3], double* off, int64_t* steps) {
+    for (int k = 0; k < 3; ++k) ext[k] = 1.0 / s->pb.inv[k];
+    if (off) *off = s->pb.delta;
+    if (steps) *steps = s->pb.le_steps;
+}

@@ -62,6 +62,11 @@ typedef struct {
     const orc_line* lines;
     double grid_cell_size;          /* 0 = 2 r_max (1+1e-6) */
     int32_t contact_capacity;
+    /* Beyond the reference: periodic axes (bit 0 x, 1 y,
+     * 2 z) and a Lees-Edwards shear rate (flow x, gradient y; needs x and y periodic). 0, 0 is
+     * the reference's walled box, bit for bit. */
+    uint32_t periodic;
+    double shear_rate;
 } orc_config;
 
 typedef struct {
@@ -157,6 +162,8 @@ void orc_sim_get_keys(const orc_sim* s, uint32_t* sorted_keys);
 int64_t orc_sim_history_count(const orc_sim* s);
 void orc_sim_get_history(const orc_sim* s, orc_hist* out);
 void orc_sim_get_grid(const orc_sim* s, orc_grid* g);
+/* periodic box of a simulation: cell extents per axis and the current Lees-Edwards offset */
+void orc_sim_get_pbox(const orc_sim* s, double cell_extent[3], double* shear_offset, int64_t* shear_steps);
 
 #ifdef __cplusplus
 }

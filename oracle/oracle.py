@@ -46,7 +46,7 @@ class orc_config(C.Structure):
                 ("pair_restitution", PD), ("rect_count", C.c_uint32),
                 ("rects", C.POINTER(orc_rect)), ("line_count", C.c_uint32),
                 ("lines", C.POINTER(orc_line)), ("grid_cell_size", C.c_double),
-                ("contact_capacity", C.c_int32)]
+                ("contact_capacity", C.c_int32), ("periodic", C.c_uint32), ("shear_rate", C.c_double)]
 
 
 class orc_grid(C.Structure):
@@ -103,6 +103,8 @@ class CConfig:
         c.lines = self.lines
         c.grid_cell_size = cfg.grid_cell_size
         c.contact_capacity = cfg.contact_capacity
+        c.periodic = getattr(cfg, "periodic", 0)
+        c.shear_rate = getattr(cfg, "shear_rate", 0.0)
         self.c = c
 
 
@@ -193,6 +195,7 @@ class Oracle:
         L.orc_sim_history_count.argtypes = [C.c_void_p]
         L.orc_sim_get_history.argtypes = [C.c_void_p, C.POINTER(orc_hist)]
         L.orc_sim_get_grid.argtypes = [C.c_void_p, C.POINTER(orc_grid)]
+        L.orc_sim_get_pbox.argtypes = [C.c_void_p, PD, PD, C.POINTER(C.c_int64)]
 
     # -- pure functions --
     def restitution_alpha(self, e):
@@ -369,6 +372,12 @@ class OracleSim:
         g = orc_grid()
         self.o.L.orc_sim_get_grid(self.h, C.byref(g))
         return g
+
+    def pbox(self):
+        """(cell extent per axis, Lees-Edwards offset, integrates so far)"""
+        ext, off, st = D3(), C.c_double(), C.c_int64()
+        self.o.L.orc_sim_get_pbox(self.h, ext, C.byref(off), C.byref(st))
+        return tuple(ext), off.value, st.value
 
 
 # ---------------------------------------------------------------------------------------------

@@ -8,7 +8,8 @@ from . import _capi
 from .simulation import (BASELINE, TWO_PHASE, CapacityError, ConfigError, ContactEntry,
                          DegenerateContactError, DeviceError, ForceAccumulator, Grid, KernelError,
                          LineWall, MaterialParams, MaterialTable, ParticleSet, RectWall, SimConfig,
-                         Simulation, StepMetrics, device_kernel_names, gen_packing, packing_config,
+                         Simulation, StepMetrics, device_kernel_names, gen_packing, gen_periodic_packing,
+                         packing_config, periodic_config,
                          total_kinetic_energy, total_momentum, wall_id)
 
 PHASE_INTEGRATE = _capi.PHASE_INTEGRATE

@@ -49,7 +49,7 @@ class dem_config(C.Structure):
                 ("rect_wall_count", C.c_uint32), ("rect_walls", C.POINTER(dem_rect_wall)),
                 ("line_wall_count", C.c_uint32), ("line_walls", C.POINTER(dem_line_wall)),
                 ("grid_cell_size", C.c_double), ("contact_capacity", C.c_int32),
-                ("collide_variant", C.c_int32)]
+                ("collide_variant", C.c_int32), ("periodic", C.c_uint32), ("shear_rate", C.c_double)]
 
 
 class dem_particles(C.Structure):
@@ -94,6 +94,7 @@ SIGNATURES = [
     ("dem_get_forces", C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     ("dem_set_forces", C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     ("dem_get_grid", C.c_int, [_P, C.POINTER(dem_grid)]),
+    ("dem_get_periodic_box", C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     ("dem_get_order", C.c_int, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     ("dem_get_contacts", C.c_int64, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_int32),
                                      C.POINTER(C.c_double), C.c_int64]),

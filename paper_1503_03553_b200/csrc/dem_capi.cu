@@ -45,6 +45,9 @@ struct dem_ctx {
     int K = 16;
     int collide_variant = 1;
     dem_grid grid{};
+    uint32_t periodic = 0;
+    double shear_rate = 0.0;
+    double cell_extent[3] = {0, 0, 0};
     uint64_t n = 0;
     uint32_t M = 0;
     size_t cap = 0;
@@ -161,6 +164,12 @@ int validate(const dem_config* cfg, const dem_particles* p, std::string* why) {
         if (!(m.sliding_friction >= 0.0)) return fail(w + "mu_d: must be >= 0");
     }
     if (cfg->grid_cell_size < 0.0) return fail("grid.cell_size: must be > 0");
+    if (cfg->periodic & ~7u) return fail("periodic: bits 0-2 (x, y, z) only");
+    if (!std::isfinite(cfg->shear_rate)) return fail("shear_rate: must be finite");
+    if (cfg->shear_rate != 0.0 && (cfg->periodic & 3u) != 3u)
+        return fail("shear_rate: Lees-Edwards shear needs periodic x and y");
+    if (cfg->periodic && cfg->collide_variant == 0)
+        return fail("periodic boxes run the two_phase collide variant");
     if (cfg->contact_capacity < 1) return fail("contacts.capacity: must be >= 1");
     if (cfg->contact_capacity > 384) return fail("contacts.capacity: B200 build supports at most 384");
     if (cfg->rect_wall_count + cfg->line_wall_count > static_cast<uint32_t>(kMaxWalls)) return fail("too many walls (max 64)");
@@ -206,6 +215,16 @@ int make_grid(const dem_config* cfg, double r_max, dem_grid* g, std::string* why
     g->nx = std::max(1, static_cast<int>(std::ceil(ex / h)));
     g->ny = std::max(1, static_cast<int>(std::ceil(ey / h)));
     g->nz = std::max(1, static_cast<int>(std::ceil(ez / h)));
+    // periodic axes: n = floor(L / h) cells of extent L / n >= h
+    const double ext[3] = {ex, ey, ez};
+    int32_t* dims[3] = {&g->nx, &g->ny, &g->nz};
+    for (int a = 0; a < 3; ++a) {
+        if (!(cfg->periodic & (1u << a))) continue;
+        const int na = static_cast<int>(std::floor(ext[a] / h));
+        if (na < 3) { *why = "periodic axis needs at least 3 cells (domain length >= 3 h)"; return DEM_ERR_CONFIG; }
+        if (a == 0 && cfg->shear_rate != 0.0 && na < 4) { *why = "sheared box needs at least 4 cells along x"; return DEM_ERR_CONFIG; }
+        *dims[a] = na;
+    }
     const int64_t cells = static_cast<int64_t>(g->nx) * g->ny * g->nz;
     if (cells > (int64_t{1} << 31)) { *why = "grid has more than 2^31 cells; increase grid.cell_size"; return DEM_ERR_CONFIG; }
     if (cells >= (int64_t{1} << 31) - 1) { *why = "grid too large for 32-bit cell keys"; return DEM_ERR_CONFIG; }
@@ -217,6 +236,17 @@ double restitution_alpha(double restitution) {  // contact_mechanics.cpp:7-12
     const double ln_eps = std::log(restitution);
     constexpr double pi = 3.14159265358979323846;
     return -2.0 * ln_eps / std::sqrt(pi * pi + ln_eps * ln_eps);
+}
+
+// periodic box fields of a context: cell extent L / n on periodic axes
+void set_periodic(dem_ctx* c, const dem_config* cfg) {
+    c->periodic = cfg->periodic & 7u;
+    c->shear_rate = c->periodic ? cfg->shear_rate : 0.0;
+    const int n[3] = {c->grid.nx, c->grid.ny, c->grid.nz};
+    for (int a = 0; a < 3; ++a) {
+        const double L = cfg->domain_max[a] - cfg->domain_min[a];
+        c->cell_extent[a] = (c->periodic & (1u << a)) ? L / static_cast<double>(n[a]) : c->grid.cell_size;
+    }
 }
 
 StepParams make_params(const dem_ctx* c, uint32_t flags) {
@@ -239,6 +269,17 @@ StepParams make_params(const dem_ctx* c, uint32_t flags) {
     p.det_lo = 1.0 - 0x1p-40;  // see k_detect
     p.det_hi = 1.0 + 0x1p-40;
     p.det_tiny = 4e-24;
+    p.periodic = c->periodic;
+    const double inv[3] = {1.0 / c->cell_extent[0], 1.0 / c->cell_extent[1], 1.0 / c->cell_extent[2]};
+    p.inv_x = (c->periodic & 1u) ? inv[0] : p.inv_h;
+    p.inv_y = (c->periodic & 2u) ? inv[1] : p.inv_h;
+    p.inv_z = (c->periodic & 4u) ? inv[2] : p.inv_h;
+    p.Lx = c->domain_max[0] - c->domain_min[0];
+    p.Ly = c->domain_max[1] - c->domain_min[1];
+    p.Lz = c->domain_max[2] - c->domain_min[2];
+    p.half_x = 0.5 * p.Lx; p.half_y = 0.5 * p.Ly; p.half_z = 0.5 * p.Lz;
+    p.shear_rate = c->shear_rate;
+    p.shear_u = c->shear_rate * p.Ly;
     p.pairs = c->d_pairs;
     p.rects = c->d_rects;
     p.lines = c->d_lines;
@@ -282,7 +323,7 @@ void enqueue_phase(const dem_ctx* c, uint32_t flags, uint64_t phase, cudaEvent_t
     const PhaseBufs b = make_bufs(c, phase);
     cudaStream_t s = c->stream;
     if (ev) cudaEventRecord(ev[0], s);
-    launch_phase_begin(b, s);
+    launch_phase_begin(p, b, s);
     if (ev) cudaEventRecord(ev[1], s);
     launch_integrate_hash(p, b, (flags & DEM_PHASE_INTEGRATE) != 0, s);
     if (ev) cudaEventRecord(ev[2], s);
@@ -587,6 +628,7 @@ int dem_create(const dem_config* cfg, const dem_particles* particles, int device
     ctx->K = cfg->contact_capacity;
     ctx->collide_variant = cfg->collide_variant;
     ctx->grid = grid;
+    set_periodic(ctx, cfg);
     ctx->n = particles->count;
     ctx->kz0 = 0;
     ctx->nz_loc = grid.nz;
@@ -630,6 +672,8 @@ int dem_clone(const dem_ctx* src, dem_ctx** out) {
     ctx->rects = src->rects; ctx->lines = src->lines;
     ctx->grid_cell_size = src->grid_cell_size; ctx->K = src->K; ctx->collide_variant = src->collide_variant;
     ctx->grid = src->grid; ctx->n = src->n; ctx->M = src->M;
+    ctx->periodic = src->periodic; ctx->shear_rate = src->shear_rate;
+    std::memcpy(ctx->cell_extent, src->cell_extent, sizeof(ctx->cell_extent));
     ctx->kz0 = src->kz0; ctx->nz_loc = src->nz_loc;
     int rc = allocate(ctx);
     if (rc == DEM_OK) {
@@ -700,6 +744,7 @@ int dem_force_phase(dem_ctx* ctx, uint32_t flags, dem_step_metrics* m) {
 
 int dem_set_collide_variant(dem_ctx* ctx, int variant) {
     if (!ctx || (variant != 0 && variant != 1)) return DEM_ERR_ARGUMENT;
+    if (ctx->periodic && variant == 0) return set_error(ctx, DEM_ERR_CONFIG, -1, 0, 0, ctx->step_index, "periodic boxes run the two_phase collide variant");
     if (ctx->collide_variant == variant) return DEM_OK;
     ctx->collide_variant = variant;
     cudaSetDevice(ctx->device);
@@ -782,6 +827,16 @@ int dem_get_grid(const dem_ctx* ctx, dem_grid* out) {
     return DEM_OK;
 }
 
+int dem_get_periodic_box(dem_ctx* ctx, double cell_extent[3], double* shear_offset) {
+    if (!ctx) return DEM_ERR_ARGUMENT;
+    if (cell_extent) for (int a = 0; a < 3; ++a) cell_extent[a] = ctx->cell_extent[a];
+    if (shear_offset) {
+        cudaSetDevice(ctx->device);
+        CUDA_TRY(cudaMemcpy(shear_offset, &ctx->ctl->le_delta, sizeof(double), cudaMemcpyDeviceToHost));
+    }
+    return DEM_OK;
+}
+
 int dem_get_order(dem_ctx* ctx, uint32_t* sorted_keys, uint32_t* permutation) {
     if (!ctx) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
@@ -820,7 +875,7 @@ int64_t dem_get_contacts(dem_ctx* ctx, uint32_t* owner_slot, int32_t* partner, d
 }
 
 int64_t dem_get_traces(dem_ctx* ctx, uint64_t* offsets, dem_trace_event* events, int64_t capacity) {
-    if (!ctx || ctx->slab || ctx->phase_count == 0 || ctx->replaced_at == ctx->phase_count) return -DEM_ERR_ARGUMENT;
+    if (!ctx || ctx->slab || ctx->periodic || ctx->phase_count == 0 || ctx->replaced_at == ctx->phase_count) return -DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
     const uint64_t n = ctx->n;
     if (n == 0) {
@@ -973,6 +1028,10 @@ int dem_create_slab(const dem_config* cfg, const dem_particles* owned, int devic
     *out = nullptr;
     std::string why;
     int rc = validate(cfg, owned, &why);
+    if (rc == DEM_OK && cfg->periodic) {
+        why = "periodic boxes run on one GPU this round (slab ring exchange not built)";
+        rc = DEM_ERR_CONFIG;
+    }
     if (rc == DEM_OK && !(cfg->grid_cell_size > 0.0)) {
         why = "grid.cell_size: a slab context needs the global cell size (2 r_max (1 + 1e-6) of all ranks)";
         rc = DEM_ERR_CONFIG;
@@ -1012,6 +1071,7 @@ int dem_create_slab(const dem_config* cfg, const dem_particles* owned, int devic
     ctx->K = cfg->contact_capacity;
     ctx->collide_variant = cfg->collide_variant;
     ctx->grid = grid;
+    set_periodic(ctx, cfg);
     ctx->slab = true;
     ctx->z_lo = z_lo;
     ctx->z_hi = z_hi;

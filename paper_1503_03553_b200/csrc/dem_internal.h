@@ -42,6 +42,12 @@ struct StepParams {
     int nrect, nline;
     uint32_t flags;      // dem_phase_flags
     double det_lo, det_hi, det_tiny;  // k_detect classification constants (kept in the param bank)
+    // periodic box (beyond the reference). periodic == 0: the reference's box.
+    uint32_t periodic;   // bit k: axis k periodic
+    double inv_x, inv_y, inv_z;  // 1 / cell extent per axis (all inv_h when nothing is periodic)
+    double Lx, Ly, Lz;           // box lengths
+    double half_x, half_y, half_z;
+    double shear_rate, shear_u;  // Lees-Edwards rate and image velocity rate * Ly
     const MatPairH* pairs;  // nmat*nmat, [owner][partner]
     const RectW* rects;
     const LineW* lines;
@@ -65,6 +71,8 @@ struct DevCtl {
     unsigned int odd_radius;                    // a radius outside [1e-100, 1e100] (or NaN) was binned
     unsigned int poly;                          // a radius != r_ref was binned this phase
     double r_ref;                               // a radius of the state (set on upload)
+    long long le_steps;                         // integrating phases so far (Lees-Edwards clock)
+    double le_delta;                            // Lees-Edwards image offset of the upper box
 };
 
 // Structure-of-arrays particle state for one buffer (sorted slot order).
@@ -143,7 +151,7 @@ inline uint32_t scan_tiles(uint32_t M) { return (M + kScanThreads * kScanItems -
 inline uint32_t detect_tiles(uint32_t n) { return ((n + kDetectThreads - 1) / kDetectThreads) * (kDetectThreads / 32); }
 
 // Launchers (dem_kernels.cu). Each enqueues exactly one kernel on `s`.
-void launch_phase_begin(const PhaseBufs& b, cudaStream_t s);
+void launch_phase_begin(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
 void launch_integrate_hash(const StepParams& p, const PhaseBufs& b, bool integrate, cudaStream_t s);
 void launch_scan_cells(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
 void launch_scatter(const StepParams& p, const PhaseBufs& b, cudaStream_t s);

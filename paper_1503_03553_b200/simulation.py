@@ -145,6 +145,9 @@ class SimConfig:  # sim_config.hpp:42-63 (fields the step reads)
     grid_cell_size: float = 0.0
     contact_capacity: int = 16
     collide_variant: int = TWO_PHASE
+    # beyond the reference: periodic axes bit 0 x, 1 y, 2 z; Lees-Edwards rate
+    periodic: int = 0
+    shear_rate: float = 0.0
 
 
 class ParticleSet:  # particle_set.hpp:13-37, numpy SoA
@@ -311,6 +314,8 @@ class _Config:
         c.grid_cell_size = cfg.grid_cell_size
         c.contact_capacity = cfg.contact_capacity
         c.collide_variant = cfg.collide_variant
+        c.periodic = getattr(cfg, "periodic", 0)
+        c.shear_rate = getattr(cfg, "shear_rate", 0.0)
         self.c = c
 
 
@@ -434,6 +439,13 @@ class Simulation:
         self._check(self._lib.dem_set_forces(self._ctx, f.ctypes.data_as(C.POINTER(C.c_double)),
                                              t.ctypes.data_as(C.POINTER(C.c_double))))
 
+    def periodic_box(self):
+        """(cell extent per axis, Lees-Edwards image offset) — DESIGN.md §6."""
+        ext = (C.c_double * 3)()
+        off = C.c_double()
+        self._check(self._lib.dem_get_periodic_box(self._ctx, ext, C.byref(off)))
+        return tuple(ext), off.value
+
     def grid(self) -> Grid:
         g = _capi.dem_grid()
         self._check(self._lib.dem_get_grid(self._ctx, C.byref(g)))
@@ -521,6 +533,19 @@ def gen_packing(n: int, s: float = 1.8, jit: float = 0.2, poly: bool = False, se
     return ps, tuple(dm)
 
 
+def gen_periodic_packing(n: int, s: float = 1.8, jit: float = 0.2, poly: bool = False, seed: int = 1,
+                         omega_half: float = 0.5):
+    """G(N, s, jit, poly, seed) laid out for a periodic box: the same
+    draws as gen_packing, the lattice starting at the origin, positions wrapped into
+    [0, side*s*r0). Returns (ParticleSet, box length L)."""
+    ps, dm = gen_packing(n, s=s, jit=jit, poly=poly, seed=seed, omega_half=omega_half)
+    r0 = 0.005
+    side = int(round((dm[0] - 4.0 * r0) / (s * r0)))  # the generator's lattice side
+    L = side * s * r0
+    ps.positions = np.mod(ps.positions - 2.0 * r0, L)
+    return ps, L
+
+
 def packing_config(domain_max, poly: bool = False, dt: float = 1e-5, capacity: Optional[int] = None,
                    gravity=(0.0, 0.0, 0.0)) -> SimConfig:
     """The §8d benchmark configuration: MaterialParams defaults, g = 0, no walls, K = 16 (32 poly)."""
@@ -531,4 +556,14 @@ def packing_config(domain_max, poly: bool = False, dt: float = 1e-5, capacity: O
     cfg.domain_max = tuple(domain_max)
     cfg.materials.add("bead", MaterialParams())
     cfg.contact_capacity = capacity if capacity is not None else (32 if poly else 16)
+    return cfg
+
+
+def periodic_config(L: float, shear_rate: float = 0.0, poly: bool = False, dt: float = 1e-5,
+                    capacity: Optional[int] = None) -> SimConfig:
+    """the §8d benchmark configuration in a fully periodic box [0, L)^3,
+    with Lees-Edwards shear (flow x, gradient y) at `shear_rate`."""
+    cfg = packing_config((L, L, L), poly=poly, dt=dt, capacity=capacity)
+    cfg.periodic = 7
+    cfg.shear_rate = shear_rate
     return cfg

@@ -50,7 +50,7 @@ def test_library_is_sm100a():
 
 def test_abi_version():
     from paper_1503_03553_b200 import _capi
-    assert _capi.lib().dem_abi_version() == 1
+    assert _capi.lib().dem_abi_version() == 2
 
 
 def test_generator_deterministic_and_shaped():

@@ -280,6 +280,9 @@ StepParams make_params(const dem_ctx* c, uint32_t flags) {
     p.half_x = 0.5 * p.Lx; p.half_y = 0.5 * p.Ly; p.half_z = 0.5 * p.Lz;
     p.shear_rate = c->shear_rate;
     p.shear_u = c->shear_rate * p.Ly;
+    if (c->periodic && (!(c->periodic & 1u) || c->grid.nx >= 5) && (!(c->periodic & 2u) || c->grid.ny >= 5) &&
+        (!(c->periodic & 4u) || c->grid.nz >= 5))
+        p.flags |= kPhaseInterior;
     p.pairs = c->d_pairs;
     p.rects = c->d_rects;
     p.lines = c->d_lines;

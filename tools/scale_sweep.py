@@ -9,6 +9,7 @@ CASES = {
     "c2_262k": dict(n=262144, s=1.8, poly=False, seed=1),
     "c3_1m_poly": dict(n=1048576, s=1.4, poly=True, seed=3, omega=50.0),
     "c4_8m": dict(n=8388608, s=1.8, poly=False, seed=4),
+    "c4_8m_periodic_le": dict(n=8388608, s=1.8, poly=False, seed=4, periodic=True, shear=1.0),
     "c5_32m_s2.35": dict(n=33554432, s=2.35, poly=False, seed=5),
     "c5_32m_s2.2": dict(n=33554432, s=2.2, poly=False, seed=5),
     "c5_32m_s2.0": dict(n=33554432, s=2.0, poly=False, seed=5),
@@ -21,8 +22,12 @@ out = open("gpurun_out/sweep.jsonl", "a")
 for name in names:
     c = CASES[name]
     t0 = time.time()
-    ps, dmax = dem.gen_packing(c["n"], s=c["s"], jit=0.2, poly=c["poly"], seed=c["seed"], omega_half=c.get("omega", 0.5))
-    cfg = dem.packing_config(dmax, poly=c["poly"])
+    if c.get("periodic"):  # config 4 proper: periodic box, Lees-Edwards shear
+        ps, L = dem.gen_periodic_packing(c["n"], s=c["s"], jit=0.2, poly=c["poly"], seed=c["seed"])
+        cfg = dem.periodic_config(L, shear_rate=c["shear"], poly=c["poly"])
+    else:
+        ps, dmax = dem.gen_packing(c["n"], s=c["s"], jit=0.2, poly=c["poly"], seed=c["seed"], omega_half=c.get("omega", 0.5))
+        cfg = dem.packing_config(dmax, poly=c["poly"])
     sim = dem.Simulation(ps, cfg)
     del ps
     sim.steps(2)

@@ -114,6 +114,10 @@ typedef struct {
      * x and y periodic, n_x >= 4). Periodic boxes run the two-phase variant on one GPU. */
     uint32_t periodic;
     double shear_rate;
+    /* 0: fp64 parity mode (the reference's arithmetic, bit for bit). 1: fp32 throughput mode —
+     * the force kernel evaluates each contact in fp32 around an fp64 geometry core (displacement,
+     * distance, overlap) and sums in fp64; north_star tolerance 1e-5 relative. */
+    int32_t precision;
 } dem_config;
 
 /* ParticleSet, particle_set.hpp:13-37, flattened (Vec3 = 3 doubles). */

@@ -290,6 +290,7 @@ struct SimConfig {
     // Lees-Edwards shear rate; 0 / 0.0 is the reference's walled box
     std::uint32_t periodic = 0;
     double shear_rate = 0.0;
+    int precision = 0;  // 0 fp64 parity, 1 fp32 throughput
 };
 
 // ---- particle_set.hpp --------------------------------------------------------------------------
@@ -624,6 +625,7 @@ class Simulation {
         ccfg_.collide_variant = cfg_.run.collide_variant == CollideVariant::two_phase ? 1 : 0;
         ccfg_.periodic = cfg_.periodic;
         ccfg_.shear_rate = cfg_.shear_rate;
+        ccfg_.precision = cfg_.precision;
     }
 
     void check(int rc) const { if (rc != DEM_OK) rethrow(ctx_.get(), rc); }

@@ -49,7 +49,8 @@ class dem_config(C.Structure):
                 ("rect_wall_count", C.c_uint32), ("rect_walls", C.POINTER(dem_rect_wall)),
                 ("line_wall_count", C.c_uint32), ("line_walls", C.POINTER(dem_line_wall)),
                 ("grid_cell_size", C.c_double), ("contact_capacity", C.c_int32),
-                ("collide_variant", C.c_int32), ("periodic", C.c_uint32), ("shear_rate", C.c_double)]
+                ("collide_variant", C.c_int32), ("periodic", C.c_uint32), ("shear_rate", C.c_double),
+                ("precision", C.c_int32)]
 
 
 class dem_particles(C.Structure):

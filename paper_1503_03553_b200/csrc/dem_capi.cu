@@ -46,6 +46,7 @@ struct dem_ctx {
     int collide_variant = 1;
     dem_grid grid{};
     uint32_t periodic = 0;
+    int precision = 0;               // 0 fp64 parity, 1 fp32 throughput
     double shear_rate = 0.0;
     double cell_extent[3] = {0, 0, 0};
     uint64_t n = 0;
@@ -170,6 +171,9 @@ int validate(const dem_config* cfg, const dem_particles* p, std::string* why) {
         return fail("shear_rate: Lees-Edwards shear needs periodic x and y");
     if (cfg->periodic && cfg->collide_variant == 0)
         return fail("periodic boxes run the two_phase collide variant");
+    if (cfg->precision != 0 && cfg->precision != 1) return fail("precision: 0 (fp64) or 1 (fp32)");
+    if (cfg->precision == 1 && cfg->collide_variant == 0)
+        return fail("the fp32 throughput mode runs the two_phase collide variant");
     if (cfg->contact_capacity < 1) return fail("contacts.capacity: must be >= 1");
     if (cfg->contact_capacity > 384) return fail("contacts.capacity: B200 build supports at most 384");
     if (cfg->rect_wall_count + cfg->line_wall_count > static_cast<uint32_t>(kMaxWalls)) return fail("too many walls (max 64)");
@@ -280,6 +284,7 @@ StepParams make_params(const dem_ctx* c, uint32_t flags) {
     p.half_x = 0.5 * p.Lx; p.half_y = 0.5 * p.Ly; p.half_z = 0.5 * p.Lz;
     p.shear_rate = c->shear_rate;
     p.shear_u = c->shear_rate * p.Ly;
+    if (c->precision == 1) p.flags |= kPhaseFp32;
     if (c->periodic && (!(c->periodic & 1u) || c->grid.nx >= 5) && (!(c->periodic & 2u) || c->grid.ny >= 5) &&
         (!(c->periodic & 4u) || c->grid.nz >= 5))
         p.flags |= kPhaseInterior;
@@ -632,6 +637,7 @@ int dem_create(const dem_config* cfg, const dem_particles* particles, int device
     ctx->collide_variant = cfg->collide_variant;
     ctx->grid = grid;
     set_periodic(ctx, cfg);
+    ctx->precision = cfg->precision;
     ctx->n = particles->count;
     ctx->kz0 = 0;
     ctx->nz_loc = grid.nz;
@@ -675,7 +681,7 @@ int dem_clone(const dem_ctx* src, dem_ctx** out) {
     ctx->rects = src->rects; ctx->lines = src->lines;
     ctx->grid_cell_size = src->grid_cell_size; ctx->K = src->K; ctx->collide_variant = src->collide_variant;
     ctx->grid = src->grid; ctx->n = src->n; ctx->M = src->M;
-    ctx->periodic = src->periodic; ctx->shear_rate = src->shear_rate;
+    ctx->periodic = src->periodic; ctx->shear_rate = src->shear_rate; ctx->precision = src->precision;
     std::memcpy(ctx->cell_extent, src->cell_extent, sizeof(ctx->cell_extent));
     ctx->kz0 = src->kz0; ctx->nz_loc = src->nz_loc;
     int rc = allocate(ctx);
@@ -747,7 +753,8 @@ int dem_force_phase(dem_ctx* ctx, uint32_t flags, dem_step_metrics* m) {
 
 int dem_set_collide_variant(dem_ctx* ctx, int variant) {
     if (!ctx || (variant != 0 && variant != 1)) return DEM_ERR_ARGUMENT;
-    if (ctx->periodic && variant == 0) return set_error(ctx, DEM_ERR_CONFIG, -1, 0, 0, ctx->step_index, "periodic boxes run the two_phase collide variant");
+    if ((ctx->periodic || ctx->precision) && variant == 0)
+        return set_error(ctx, DEM_ERR_CONFIG, -1, 0, 0, ctx->step_index, "periodic boxes and the fp32 mode run the two_phase collide variant");
     if (ctx->collide_variant == variant) return DEM_OK;
     ctx->collide_variant = variant;
     cudaSetDevice(ctx->device);
@@ -1075,6 +1082,7 @@ int dem_create_slab(const dem_config* cfg, const dem_particles* owned, int devic
     ctx->collide_variant = cfg->collide_variant;
     ctx->grid = grid;
     set_periodic(ctx, cfg);
+    ctx->precision = cfg->precision;
     ctx->slab = true;
     ctx->z_lo = z_lo;
     ctx->z_hi = z_hi;

@@ -15,6 +15,7 @@ constexpr uint32_t kWallBit = 0x80000000u;  // partner codes >= this are walls: 
 constexpr unsigned long long kNoError = ~0ull;
 constexpr uint32_t kPhaseSlab = 64u;  // internal phase flag: slab context (ghost-aware kernels)
 constexpr uint32_t kPhaseInterior = 128u;  // internal: every periodic axis has >= 5 cells (k_detect)
+constexpr uint32_t kPhaseFp32 = 256u;      // internal: fp32 throughput mode (k_force_reduce)
 
 struct MatPairH {  // host mirror of MatPair (dem_math.cuh)
     double shear_sum, young_sum, alpha, mu;

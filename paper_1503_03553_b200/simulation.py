@@ -148,6 +148,8 @@ class SimConfig:  # sim_config.hpp:42-63 (fields the step reads)
     # beyond the reference: periodic axes bit 0 x, 1 y, 2 z; Lees-Edwards rate
     periodic: int = 0
     shear_rate: float = 0.0
+    # 0 fp64 parity mode (bitwise with the reference), 1 fp32 throughput mode (1e-5)
+    precision: int = 0
 
 
 class ParticleSet:  # particle_set.hpp:13-37, numpy SoA
@@ -316,6 +318,7 @@ class _Config:
         c.collide_variant = cfg.collide_variant
         c.periodic = getattr(cfg, "periodic", 0)
         c.shear_rate = getattr(cfg, "shear_rate", 0.0)
+        c.precision = getattr(cfg, "precision", 0)
         self.c = c
 
 

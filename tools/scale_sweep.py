@@ -7,6 +7,8 @@ import paper_1503_03553_b200 as dem
 
 CASES = {
     "c2_262k": dict(n=262144, s=1.8, poly=False, seed=1),
+    "c2_262k_fp32": dict(n=262144, s=1.8, poly=False, seed=1, precision=1),
+    "c5_32m_s1.8_fp32": dict(n=33554432, s=1.8, poly=False, seed=5, precision=1),
     "c3_1m_poly": dict(n=1048576, s=1.4, poly=True, seed=3, omega=50.0),
     "c4_8m": dict(n=8388608, s=1.8, poly=False, seed=4),
     "c4_8m_periodic_le": dict(n=8388608, s=1.8, poly=False, seed=4, periodic=True, shear=1.0),
@@ -28,6 +30,7 @@ for name in names:
     else:
         ps, dmax = dem.gen_packing(c["n"], s=c["s"], jit=0.2, poly=c["poly"], seed=c["seed"], omega_half=c.get("omega", 0.5))
         cfg = dem.packing_config(dmax, poly=c["poly"])
+    cfg.precision = c.get("precision", 0)
     sim = dem.Simulation(ps, cfg)
     del ps
     sim.steps(2)

@@ -1038,10 +1038,6 @@ int dem_create_slab(const dem_config* cfg, const dem_particles* owned, int devic
     *out = nullptr;
     std::string why;
     int rc = validate(cfg, owned, &why);
-    if (rc == DEM_OK && cfg->periodic) {
-        why = "periodic boxes run on one GPU this round (slab ring exchange not built)";
-        rc = DEM_ERR_CONFIG;
-    }
     if (rc == DEM_OK && !(cfg->grid_cell_size > 0.0)) {
         why = "grid.cell_size: a slab context needs the global cell size (2 r_max (1 + 1e-6) of all ranks)";
         rc = DEM_ERR_CONFIG;
@@ -1086,8 +1082,11 @@ int dem_create_slab(const dem_config* cfg, const dem_particles* owned, int devic
     ctx->slab = true;
     ctx->z_lo = z_lo;
     ctx->z_hi = z_hi;
-    ctx->kz0 = std::max(z_lo - 1, 0);
-    ctx->nz_loc = std::min(z_hi + 1, grid.nz) - ctx->kz0;
+    // keyed planes: the slab plus one ghost plane each side (beyond the grid only if z is periodic,
+    // where the neighbours form a ring)
+    const bool zring = (cfg->periodic & 4u) != 0;
+    ctx->kz0 = zring ? z_lo - 1 : std::max(z_lo - 1, 0);
+    ctx->nz_loc = (zring ? z_hi + 1 : std::min(z_hi + 1, grid.nz)) - ctx->kz0;
     ctx->M = static_cast<uint32_t>(static_cast<int64_t>(grid.nx) * grid.ny * ctx->nz_loc);
     ctx->n = owned->count;
     ctx->n_cap = std::max<uint64_t>(capacity, owned->count) + 32;
@@ -1184,8 +1183,8 @@ int dem_slab_ghosts(dem_ctx* ctx, const void* recs_lo, uint64_t n_lo, const void
         return set_error(ctx, DEM_ERR_CAPACITY, -1, 0, 0, ctx->step_index, "slab: context capacity exceeded by ghosts");
     cudaSetDevice(ctx->device);
     const SlabBufs s = make_slab(ctx, nullptr, nullptr, 0);
-    launch_slab_ghosts(s, recs_lo, static_cast<uint32_t>(n_lo), static_cast<uint32_t>(ctx->n_own), ctx->stream);
-    launch_slab_ghosts(s, recs_hi, static_cast<uint32_t>(n_hi), static_cast<uint32_t>(ctx->n_own + n_lo), ctx->stream);
+    launch_slab_ghosts(s, recs_lo, static_cast<uint32_t>(n_lo), static_cast<uint32_t>(ctx->n_own), false, ctx->stream);
+    launch_slab_ghosts(s, recs_hi, static_cast<uint32_t>(n_hi), static_cast<uint32_t>(ctx->n_own + n_lo), true, ctx->stream);
     ctx->n_asm = ctx->n_own + n_lo + n_hi;
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     CUDA_TRY(cudaGetLastError());

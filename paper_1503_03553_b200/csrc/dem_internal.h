@@ -142,7 +142,7 @@ struct SlabBufs {
 void launch_slab_migrate(const StepParams& p, const SlabBufs& s, bool integrate, cudaStream_t st);
 void launch_slab_import(const SlabBufs& s, const void* recs, uint32_t n, uint32_t base, size_t imp_off, cudaStream_t st);
 void launch_slab_halo(const StepParams& p, const SlabBufs& s, uint32_t n_own, cudaStream_t st);
-void launch_slab_ghosts(const SlabBufs& s, const void* recs, uint32_t n, uint32_t base, cudaStream_t st);
+void launch_slab_ghosts(const SlabBufs& s, const void* recs, uint32_t n, uint32_t base, bool from_hi, cudaStream_t st);
 
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;

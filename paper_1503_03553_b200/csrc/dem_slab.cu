@@ -17,12 +17,14 @@
 
 #include "dem_internal.h"
 #include "dem_math.cuh"
+#include "dem_periodic.cuh"
 
 namespace demb200 {
 
 namespace {
 
 constexpr uint32_t kGhost = 0x80000000u;
+constexpr uint32_t kGhostHi = 0x40000000u;  // the halo copy came from the z_hi side
 
 __device__ __forceinline__ void raise_err(DevCtl* ctl, int kernel, uint32_t slot, uint32_t id, int code) {
     const unsigned long long key = (static_cast<unsigned long long>(kernel) << 56) |
@@ -34,7 +36,7 @@ __device__ __forceinline__ void raise_err(DevCtl* ctl, int kernel, uint32_t slot
 
 // global cell plane of a position: the z part of calc_hash (grid.cpp:30-52)
 __device__ __forceinline__ int cell_z(const StepParams& p, double z) {
-    int cz = to_int_x86(floor((z - p.oz) * p.inv_h));
+    int cz = to_int_x86(floor((z - p.oz) * p.inv_z));
     return cz < 0 ? 0 : (cz >= p.nz ? p.nz - 1 : cz);
 }
 
@@ -90,8 +92,18 @@ __global__ void __launch_bounds__(256) k_slab_migrate(StepParams p, SlabBufs s) 
             om.x = om.x + t.x * s2; om.y = om.y + t.y * s2; om.z = om.z + t.z * s2;
         }
     }
-    const int cz = cell_z(p, pr.z);
-    const int cls = cz < s.z_lo ? 1 : (cz >= s.z_hi ? 2 : 0);
+    int cls;
+    if (p.periodic) {
+        // periodic z: the direction comes from the unwrapped plane (a particle leaving the top of
+        // the last slab goes up the ring, to slab 0), then the position is wrapped
+        int cz = cell_z(p, pr.z);
+        if (p.periodic & 4u) cz = to_int_x86(floor((pr.z - p.oz) * p.inv_z));
+        if (INTEGRATE) wrap_periodic(p, s.ctl->le_delta, pr, vm);
+        cls = cz < s.z_lo ? 1 : (cz >= s.z_hi ? 2 : 0);
+    } else {
+        const int cz = cell_z(p, pr.z);
+        cls = cz < s.z_lo ? 1 : (cz >= s.z_hi ? 2 : 0);
+    }
     const uint32_t slot = agg_add(&s.counters[cls], cls);
     const uint32_t hpos = s.H_old.pos[i], hcnt = s.H_old.cnt[i];
     if (cls == 0) {
@@ -137,6 +149,12 @@ __global__ void __launch_bounds__(256) k_slab_import(SlabBufs s, const uint8_t* 
     s.hrm_cnt[base + t] = hcnt;
 }
 
+// the Lees-Edwards clock advances with the integrating migrate (the slab force phase does not
+// integrate)
+__global__ void k_le_advance(StepParams p, DevCtl* ctl) {
+    if (threadIdx.x == 0 && ctl->err_key == kNoError) le_clock(p, ctl, true);
+}
+
 // owned particles of Y[0, n_own) on the boundary planes become ghost records for the neighbours
 __global__ void __launch_bounds__(256) k_slab_halo(StepParams p, SlabBufs s, uint32_t n_own) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -159,13 +177,14 @@ __global__ void __launch_bounds__(256) k_slab_halo(StepParams p, SlabBufs s, uin
     }
 }
 
-__global__ void __launch_bounds__(256) k_slab_ghosts(SlabBufs s, const uint8_t* recs, uint32_t n, uint32_t base) {
+__global__ void __launch_bounds__(256) k_slab_ghosts(SlabBufs s, const uint8_t* recs, uint32_t n, uint32_t base,
+                                                      bool from_hi) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
     const uint8_t* rec = recs + static_cast<size_t>(t) * s.ghost_bytes;
     const double4* d = reinterpret_cast<const double4*>(rec);
     uint2 idm = *reinterpret_cast<const uint2*>(rec + 96);
-    idm.y |= kGhost;
+    idm.y |= kGhost | (from_hi ? kGhostHi : 0u);
     put_state(s.Y, base + t, ld4(&d[0]), ld4(&d[1]), ld4(&d[2]), idm);
     s.hrm_pos[base + t] = 0;
     s.hrm_cnt[base + t] = 0;
@@ -176,6 +195,7 @@ inline unsigned blocks(size_t n) { return static_cast<unsigned>((n + 255) / 256)
 }  // namespace
 
 void launch_slab_migrate(const StepParams& p, const SlabBufs& s, bool integrate, cudaStream_t st) {
+    if (integrate && p.periodic) k_le_advance<<<1, 32, 0, st>>>(p, s.ctl);
     if (!s.n_x) return;
     if (integrate) k_slab_migrate<true><<<blocks(s.n_x), 256, 0, st>>>(p, s);
     else k_slab_migrate<false><<<blocks(s.n_x), 256, 0, st>>>(p, s);
@@ -186,8 +206,8 @@ void launch_slab_import(const SlabBufs& s, const void* recs, uint32_t n, uint32_
 void launch_slab_halo(const StepParams& p, const SlabBufs& s, uint32_t n_own, cudaStream_t st) {
     if (n_own) k_slab_halo<<<blocks(n_own), 256, 0, st>>>(p, s, n_own);
 }
-void launch_slab_ghosts(const SlabBufs& s, const void* recs, uint32_t n, uint32_t base, cudaStream_t st) {
-    if (n) k_slab_ghosts<<<blocks(n), 256, 0, st>>>(s, static_cast<const uint8_t*>(recs), n, base);
+void launch_slab_ghosts(const SlabBufs& s, const void* recs, uint32_t n, uint32_t base, bool from_hi, cudaStream_t st) {
+    if (n) k_slab_ghosts<<<blocks(n), 256, 0, st>>>(s, static_cast<const uint8_t*>(recs), n, base, from_hi);
 }
 
 }  // namespace demb200

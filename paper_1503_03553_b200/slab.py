@@ -40,14 +40,19 @@ GHOST_BIT = 0x80000000
 class GlobalGrid:
     oz: float
     h: float
-    inv_h: float
+    inv_h: float      # 1 / cell extent along z
     nz: int
+    ring: bool = False  # periodic z: slab neighbours form a ring
 
 
 def global_grid(cfg: SimConfig, r_max: float) -> GlobalGrid:
-    """make_grid (grid.cpp:10-28) for the z axis, with the cell size every rank must share."""
+    """make_grid (grid.cpp:10-28) for the z axis, with the cell size every rank must share; a
+    periodic z gets floor(L/h) cells of extent L/n."""
     h = cfg.grid_cell_size if cfg.grid_cell_size > 0.0 else 2.0 * r_max * (1.0 + 1e-6)
     ez = cfg.domain_max[2] - cfg.domain_min[2]
+    if getattr(cfg, "periodic", 0) & 4:
+        nz = int(math.floor(ez / h))
+        return GlobalGrid(cfg.domain_min[2], h, 1.0 / (ez / nz), nz, True)
     nz = max(1, int(math.ceil(ez / h)))
     return GlobalGrid(cfg.domain_min[2], h, 1.0 / h, nz)
 
@@ -91,8 +96,9 @@ class LoopbackTransport:
     """Several ranks in one process (e.g. on one GPU): records are copied between the ranks'
     buffers directly. Used to validate the decomposition on a single device."""
 
-    def __init__(self, ranks):
+    def __init__(self, ranks, ring: bool = False):
         self.ranks = ranks
+        self.ring = ring  # periodic z: rank 0 and rank R-1 are neighbours
 
     def exchange(self, kind: str):
         R = len(self.ranks)
@@ -100,58 +106,76 @@ class LoopbackTransport:
             rk.recv_count[kind] = [0, 0]
         for r, rk in enumerate(self.ranks):
             n_lo, n_hi = rk.send_count[kind]
-            if r > 0 and n_lo:  # to r-1, which receives it from above
-                self.ranks[r - 1].receive(kind, 1, rk.send_view(kind, 0, n_lo), n_lo)
-            if r < R - 1 and n_hi:
-                self.ranks[r + 1].receive(kind, 0, rk.send_view(kind, 1, n_hi), n_hi)
+            lo, hi = r - 1, r + 1
+            if self.ring:
+                lo, hi = lo % R, hi % R
+            if 0 <= lo and n_lo:  # to the rank below, which receives it from above
+                self.ranks[lo].receive(kind, 1, rk.send_view(kind, 0, n_lo), n_lo)
+            if hi < R and n_hi:
+                self.ranks[hi].receive(kind, 0, rk.send_view(kind, 1, n_hi), n_hi)
 
 
 class TorchTransport:
     """One rank per process over torch.distributed: counts, then payloads, to the z-neighbours
-    with batched isend/irecv (NCCL P2P over NVLink for device buffers; gloo for CPU buffers)."""
+    with batched isend/irecv (NCCL P2P over NVLink for device buffers; gloo for CPU buffers).
+    Each exchange is two half-exchanges — every rank sends up (its hi buffer) and receives from
+    below, then sends down and receives from above — so that on a ring of 2 ranks, where the
+    neighbour below and above are the same process, the two messages cannot be confused."""
 
-    def __init__(self, rank: int, world: int):
+    def __init__(self, rank: int, world: int, ring: bool = False):
         import torch
         import torch.distributed as dist
         self.torch, self.dist = torch, dist
         self.rank, self.world = rank, world
+        self.ring = ring
         self.ranks = None
 
     def bind(self, rk):
         self.ranks = [rk]
 
-    def exchange(self, kind: str):
+    def _half(self, rk, kind, dev, send_side, to, frm):
+        """send buffer `send_side` to rank `to` (None: nobody), receive into the opposite side
+        from rank `frm` (None: nobody); returns the received count."""
         torch, dist = self.torch, self.dist
+        recv_side = 1 - send_side
+        n_send = rk.send_count[kind][send_side]
+        c_send = torch.tensor([n_send], dtype=torch.int64, device=dev)
+        c_recv = torch.zeros(1, dtype=torch.int64, device=dev)
+        ops = []
+        if to is not None:
+            ops.append(dist.P2POp(dist.isend, c_send, to))
+        if frm is not None:
+            ops.append(dist.P2POp(dist.irecv, c_recv, frm))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        m = int(c_recv[0].item()) if frm is not None else 0
+        ops = []
+        if to is not None and n_send:
+            ops.append(dist.P2POp(dist.isend, rk.send_view(kind, send_side, n_send), to))
+        if frm is not None and m:
+            ops.append(dist.P2POp(dist.irecv, rk.recv_view(kind, recv_side, m), frm))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        return m
+
+    def exchange(self, kind: str):
         rk = self.ranks[0]
         dev = rk.buffer_device()
-        n_lo, n_hi = rk.send_count[kind]
-        lo, hi = self.rank - 1, self.rank + 1
-        c_send = [torch.tensor([n_lo], dtype=torch.int64, device=dev), torch.tensor([n_hi], dtype=torch.int64, device=dev)]
-        c_recv = [torch.zeros(1, dtype=torch.int64, device=dev), torch.zeros(1, dtype=torch.int64, device=dev)]
-        ops = []
-        if lo >= 0:
-            ops += [dist.P2POp(dist.isend, c_send[0], lo), dist.P2POp(dist.irecv, c_recv[0], lo)]
-        if hi < self.world:
-            ops += [dist.P2POp(dist.isend, c_send[1], hi), dist.P2POp(dist.irecv, c_recv[1], hi)]
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
-        m_lo, m_hi = int(c_recv[0].item()), int(c_recv[1].item())
-        rk.recv_count[kind] = [0, 0]
-        ops = []
-        if lo >= 0 and n_lo:
-            ops.append(dist.P2POp(dist.isend, rk.send_view(kind, 0, n_lo), lo))
-        if lo >= 0 and m_lo:
-            ops.append(dist.P2POp(dist.irecv, rk.recv_view(kind, 0, m_lo), lo))
-        if hi < self.world and n_hi:
-            ops.append(dist.P2POp(dist.isend, rk.send_view(kind, 1, n_hi), hi))
-        if hi < self.world and m_hi:
-            ops.append(dist.P2POp(dist.irecv, rk.recv_view(kind, 1, m_hi), hi))
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+        R, r = self.world, self.rank
+        lo = (r - 1) % R if (self.ring or r > 0) else None
+        hi = (r + 1) % R if (self.ring or r < R - 1) else None
+        if R == 1 and self.ring:  # a ring of one: both halves come back to this rank
+            for side in (0, 1):
+                n = rk.send_count[kind][side]
+                rk.recv_view(kind, 1 - side, n).copy_(rk.send_view(kind, side, n))
+            rk.recv_count[kind] = [rk.send_count[kind][1], rk.send_count[kind][0]]
+            return
+        m_lo = self._half(rk, kind, dev, 1, hi, lo)   # up: my hi buffer -> above; from below
+        m_hi = self._half(rk, kind, dev, 0, lo, hi)   # down: my lo buffer -> below; from above
         if dev.type == "cuda":
-            torch.cuda.current_stream(dev).synchronize()
+            self.torch.cuda.current_stream(dev).synchronize()
         rk.recv_count[kind] = [m_lo, m_hi]
 
 
@@ -313,7 +337,10 @@ def build_local_slabs(ps: ParticleSet, cfg: SimConfig, nranks: int, rank_ids: Se
         z_lo, z_hi = bounds[r]
         mask = (planes >= z_lo) & (planes < z_hi)
         owned = select(ps, mask)
-        ghosts = (per_plane[z_lo - 1] if z_lo > 0 else 0) + (per_plane[z_hi] if z_hi < g.nz else 0)
+        if g.ring:
+            ghosts = per_plane[(z_lo - 1) % g.nz] + per_plane[z_hi % g.nz]
+        else:
+            ghosts = (per_plane[z_lo - 1] if z_lo > 0 else 0) + (per_plane[z_hi] if z_hi < g.nz else 0)
         capacity = int(1024 + headroom * (len(owned.ids) + ghosts))
         ranks.append(backend(scfg, owned, z_lo, z_hi, capacity, device=device))
     return ranks, bounds, g

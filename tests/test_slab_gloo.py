@@ -91,3 +91,61 @@ def test_slab_bounds_balance():
     assert all(b[k][1] == b[k + 1][0] for k in range(3))
     with pytest.raises(ValueError):
         slab_bounds(planes, 10, 11)
+
+
+class _FakeRank:
+    """Record buffers only: what TorchTransport moves (CPU tensors over gloo)."""
+
+    def __init__(self, rank):
+        import torch
+        self.rec = 8
+        self.send = {"ghost": [torch.full((64,), 10 * rank + s, dtype=torch.uint8) for s in (0, 1)]}
+        self.recv = {"ghost": [torch.zeros(64, dtype=torch.uint8) for _ in (0, 1)]}
+        self.send_count = {"ghost": [rank + 1, rank + 2]}
+        self.recv_count = {"ghost": [0, 0]}
+
+    def buffer_device(self):
+        return self.send["ghost"][0].device
+
+    def send_view(self, kind, side, n):
+        return self.send[kind][side][: n * self.rec]
+
+    def recv_view(self, kind, side, n):
+        return self.recv[kind][side][: n * self.rec]
+
+
+def _ring_worker(rank, world, port, outdir):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    for p in (here, os.path.dirname(here)):
+        if p not in sys.path:
+            sys.path.insert(0, p)
+    import torch.distributed as dist
+    from paper_1503_03553_b200.slab import TorchTransport
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rk = _FakeRank(rank)
+    tr = TorchTransport(rank, world, ring=True)
+    tr.bind(rk)
+    tr.exchange("ghost")
+    np.savez(os.path.join(outdir, f"ring{rank}.npz"), cnt=np.array(rk.recv_count["ghost"]),
+             lo=rk.recv["ghost"][0].numpy(), hi=rk.recv["ghost"][1].numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ring_transport_gloo(world):
+    """Periodic z: slab neighbours form a ring. Each rank receives, from below, the
+    hi buffer of rank r-1 mod R and, from above, the lo buffer of rank r+1 mod R — including on a
+    ring of 2, where both neighbours are the same process."""
+    import torch.multiprocessing as mp
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_ring_worker, args=(world, _free_port(), d), nprocs=world, join=True)
+        for r in range(world):
+            z = np.load(os.path.join(d, f"ring{r}.npz"))
+            lo, hi = (r - 1) % world, (r + 1) % world
+            assert list(z["cnt"]) == [lo + 2, hi + 1]
+            assert (z["lo"][: (lo + 2) * 8] == 10 * lo + 1).all()
+            assert (z["hi"][: (hi + 1) * 8] == 10 * hi + 0).all()

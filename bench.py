@@ -330,6 +330,15 @@ def run_b200(args):
             traffic = json.load(open(tpath)).get(dom)
         except Exception:
             traffic = None
+    # what actually bounds the dominant kernel (FP64 pipe / latency, not HBM): the ncu capture
+    # of the same workload committed under profiles/ (tools/profile_round.sh)
+    util = None
+    upath = os.path.join(ROOT, "profiles", "r01_kernel_util.json")
+    if os.path.exists(upath):
+        try:
+            util = json.load(open(upath)).get(dom)
+        except Exception:
+            util = None
 
     # --- e2e through the C ABI with host buffers ---
     # (pinned host arrays, as a production caller keeps them; the state goes up and comes back
@@ -364,7 +373,8 @@ def run_b200(args):
                 "how": "dem_set_particles(pinned host) + dem_step(1) + dem_get_particles(pinned host), wall clock"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_ach, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": dom_ach / peak,
-                     "traffic": traffic, "algorithmic_bytes": nbytes[dom], "ms": kms[dom]},
+                     "traffic": traffic, "algorithmic_bytes": nbytes[dom], "ms": kms[dom],
+                     "ncu": dict(util, source="profiles/r01_kernel_util.json (ncu --set full)") if util else None},
         "force_kernel": {"name": "k_force_reduce", "achieved": force_ach, "frac": force_ach / peak, "ms": kms["k_force_reduce"],
                          "algorithmic_bytes": nbytes["k_force_reduce"]},
         "kernel_ms": kms,

@@ -104,7 +104,7 @@ def main(tag):
             lines.append(f"| {k} | {len(v)} | {statistics.median(v):.0f} | {sh} |")
         lines.append("")
     rep = os.path.join(OUT, f"prof_{tag}.ncu-rep")
-    traffic = {}
+    traffic, util = {}, {}
     if os.path.exists(rep):
         hdr, units, rows = ncu_raw(rep)
         idx = {h: i for i, h in enumerate(hdr)}
@@ -140,9 +140,22 @@ def main(tag):
             rb = to_bytes(r[idx["dram__bytes_read.sum"]], units[idx["dram__bytes_read.sum"]])
             wb = to_bytes(r[idx["dram__bytes_write.sum"]], units[idx["dram__bytes_write.sum"]])
             traffic[name] = rb + wb
+
+            def num(m):
+                try:
+                    return float(r[idx[m]])
+                except (KeyError, ValueError):
+                    return None
+            tpi = num("smsp__thread_inst_executed_per_inst_executed.ratio")
+            util[name] = {"fp64_pipe_pct": num("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                          "warp_exec_efficiency": tpi / 32.0 if tpi else None,
+                          "dram_pct": num("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                          "warps_active_pct": num("sm__warps_active.avg.pct_of_peak_sustained_active"),
+                          "l2_hit_pct": num("lts__t_sector_hit_rate.pct")}
         lines.append("")
         lines.append("threads/inst / 32 = warp execution efficiency. DRAM traffic is per launch (cold L2 under replay).")
         json.dump(traffic, open(os.path.join(PROF, f"{tag}_traffic.json"), "w"), indent=1)
+        json.dump(util, open(os.path.join(PROF, f"{tag}_kernel_util.json"), "w"), indent=1)
     open(os.path.join(PROF, f"{tag}_summary.md"), "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 

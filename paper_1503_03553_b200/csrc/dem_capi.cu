@@ -449,6 +449,7 @@ int allocate(dem_ctx* ctx) {
         CUDA_TRY(dalloc(ctx, &ctx->state[b].vel_m, n));
         CUDA_TRY(dalloc(ctx, &ctx->state[b].omg, n));
         CUDA_TRY(dalloc(ctx, &ctx->state[b].idm, n));
+        CUDA_TRY(dalloc(ctx, &ctx->state[b].pos_f, n));
         CUDA_TRY(dalloc(ctx, &ctx->hist[b].pos, n));
         CUDA_TRY(dalloc(ctx, &ctx->hist[b].cnt, n));
         CUDA_TRY(dalloc(ctx, &ctx->hist[b].key, ctx->cap));

@@ -83,6 +83,7 @@ struct StateBuf {
     double4* vel_m;   // vx, vy, vz, mass
     double4* omg;     // wx, wy, wz, 0
     uint2* idm;       // stable id, material id
+    float4* pos_f;    // x, y, z, radius rounded to fp32 (k_reorder; k_detect's conservative prefilter)
 };
 
 // Contacts of one force phase, tile-compacted: warp tile t (slots 32t..32t+31) owns the pair

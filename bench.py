@@ -54,8 +54,8 @@ def algorithmic_bytes(n, c, m):
         "k_integrate_hash": 252 * n,
         "k_scan_cells": 12 * m,
         "k_scatter": 24 * n,
-        "k_reorder": 236 * n,
-        "k_detect": 44 * n + 4 * m + 8 * c,
+        "k_reorder": 252 * n,
+        "k_detect": 60 * n + 4 * m + 8 * c,
         "k_force_reduce": 172 * n + 64 * c,
     }
 

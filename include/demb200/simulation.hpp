@@ -397,6 +397,7 @@ class Simulation {
     }
 
     Simulation(const Simulation& o) : cfg_(o.cfg_) {
+        o.run_pending();
         o.flush();
         build_c_config();
         dem_ctx* c = nullptr;
@@ -421,6 +422,28 @@ class Simulation {
         cfg_.run.collide_variant = v;
         check(dem_set_collide_variant(ctx_.get(), v == CollideVariant::two_phase ? 1 : 0));
     }
+    /// The reference's per-kernel methods (pipeline.hpp:77-86). The B200 step fuses kernels, so
+    /// calls compose into one force phase in pipeline order (Integrate, CalcHash, BitonicSort,
+    /// FindCellBoundsAndReorder, ZeroForces, ForceGravity, InitializeContactIDs, Collide,
+    /// CollideRectangle, CollideLine) that runs when a result is observed (particles(), forces(),
+    /// contact_table(), order(), traces(), step(), ...) or when a kernel earlier in that order is
+    /// called again. Every composed phase bins and starts from zeroed accumulators, as every
+    /// reference caller does (tests/test_pipeline.cpp:69-76, runner.cpp:261-270); errors surface
+    /// when the phase runs.
+    void kernel_integrate() { compose(0, DEM_PHASE_INTEGRATE); }
+    void kernel_calc_hash() { compose(1, 0); }
+    void kernel_bitonic_sort() { compose(2, 0); }
+    void kernel_find_cell_bounds_and_reorder() { compose(3, 0); }
+    void zero_forces() { compose(4, 0); }
+    void kernel_force_gravity() { compose(5, DEM_PHASE_GRAVITY); }
+    void kernel_initialize_contact_ids() { compose(6, 0); }
+    void kernel_collide(CollideVariant variant, bool /*record_traces: traces are produced on demand*/) {
+        compose(7, DEM_PHASE_PP);
+        pending_variant_ = variant == CollideVariant::two_phase ? 1 : 0;
+    }
+    void kernel_collide_rectangle() { compose(8, DEM_PHASE_RECT); }
+    void kernel_collide_line() { compose(9, DEM_PHASE_LINE); }
+
     /// advance_to_collide + kernel_collide (tests/test_pipeline.cpp:69-76): pp only, no gravity.
     StepMetrics advance_and_collide() {
         return run([&](dem_step_metrics* m) { return dem_force_phase(ctx_.get(), DEM_PHASE_INTEGRATE | DEM_PHASE_PP, m); }, false);
@@ -453,17 +476,22 @@ class Simulation {
     const ContactTable& contact_table() const { sync_table(); return table_; }
     const SortedOrder& order() const { sync_order(); return order_; }
     std::int64_t step_index() const { return dem_step_index(ctx_.get()); }
-    std::int64_t last_clamp_count() const { return last_.clamps; }
+    std::int64_t last_clamp_count() const { run_pending(); return last_.clamps; }
     double mean_coordination() const {
+        run_pending();
         const auto n = dem_size(ctx_.get());
         return n ? double(last_.pp_contact_events) / double(n) : 0.0;
     }
 
   private:
     struct CtxDeleter { void operator()(dem_ctx* c) const { dem_destroy(c); } };
+    std::uint32_t pending_ = 0;    // composed per-kernel calls (kernel_integrate ...)
+    int pending_last_ = -1;
+    int pending_variant_ = -1;
 
     template <typename F>
     StepMetrics run(F&& fn, bool record) {
+        if (pending_last_ >= 0) run_pending();
         flush();
         dem_step_metrics m{};
         const int rc = fn(&m);
@@ -488,6 +516,26 @@ class Simulation {
         return last_;
     }
 
+    void compose(int k, std::uint32_t flag) {
+        if (k <= pending_last_) run_pending();
+        pending_ |= flag;
+        pending_last_ = k;
+    }
+    // runs the composed force phase (see kernel_integrate); a no-op without pending kernels
+    void run_pending() const {
+        auto* self = const_cast<Simulation*>(this);
+        if (pending_last_ < 0) return;
+        const std::uint32_t flags = pending_;
+        const int variant = pending_variant_;
+        self->pending_ = 0;
+        self->pending_last_ = -1;
+        self->pending_variant_ = -1;
+        const int current = cfg_.run.collide_variant == CollideVariant::two_phase ? 1 : 0;
+        if (variant >= 0 && variant != current) self->check(dem_set_collide_variant(ctx_.get(), variant));
+        self->run([&](dem_step_metrics* m) { return dem_force_phase(ctx_.get(), flags, m); }, false);
+        if (variant >= 0 && variant != current) self->check(dem_set_collide_variant(ctx_.get(), current));
+    }
+
     void flush() const {
         auto* self = const_cast<Simulation*>(this);
         if (state_dirty_) {
@@ -502,6 +550,7 @@ class Simulation {
     }
 
     void sync_state() const {
+        run_pending();
         if (state_fresh_ || state_dirty_) return;
         auto* self = const_cast<Simulation*>(this);
         const auto n = dem_size(ctx_.get());
@@ -513,6 +562,7 @@ class Simulation {
         self->state_fresh_ = true;
     }
     void sync_forces() const {
+        run_pending();
         if (forces_fresh_ || forces_dirty_) return;
         auto* self = const_cast<Simulation*>(this);
         const auto n = dem_size(ctx_.get());
@@ -522,6 +572,7 @@ class Simulation {
         self->forces_fresh_ = true;
     }
     void sync_table() const {
+        run_pending();
         if (table_fresh_) return;
         auto* self = const_cast<Simulation*>(this);
         const auto n = static_cast<std::uint32_t>(dem_size(ctx_.get()));
@@ -542,6 +593,7 @@ class Simulation {
     }
 
     void sync_order() const {
+        run_pending();
         if (order_fresh_) return;
         auto* self = const_cast<Simulation*>(this);
         const auto n = dem_size(ctx_.get());
@@ -561,6 +613,7 @@ class Simulation {
     }
 
     void sync_traces() const {
+        run_pending();
         if (traces_fresh_) return;
         auto* self = const_cast<Simulation*>(this);
         const auto n = dem_size(ctx_.get());

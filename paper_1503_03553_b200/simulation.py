@@ -368,18 +368,72 @@ class Simulation:
         if rc != 0:
             _raise(self._lib, self._ctx, rc)
 
+    # --- the reference's per-kernel methods, pipeline.hpp:77-86 ---
+    # The B200 step fuses kernels: calls compose into one force phase in pipeline order that runs
+    # when a result is observed or a kernel earlier in that order is called again (the C++
+    # drop-in, include/demb200/simulation.hpp, does the same). Every composed phase bins and
+    # starts from zeroed accumulators; errors surface when the phase runs.
+    _ORDER = {"integrate": (0, _capi.PHASE_INTEGRATE), "calc_hash": (1, 0), "bitonic_sort": (2, 0),
+              "find_cell_bounds_and_reorder": (3, 0), "zero_forces": (4, 0),
+              "force_gravity": (5, _capi.PHASE_GRAVITY), "initialize_contact_ids": (6, 0),
+              "collide": (7, _capi.PHASE_PP), "collide_rectangle": (8, _capi.PHASE_RECT),
+              "collide_line": (9, _capi.PHASE_LINE)}
+
+    def _compose(self, name, variant=None):
+        k, flag = self._ORDER[name]
+        pend = self.__dict__.setdefault("_pending", [-1, 0, None])
+        if k <= pend[0]:
+            self._run_pending()
+            pend = self._pending
+        pend[0], pend[1] = k, pend[1] | flag
+        if variant is not None:
+            pend[2] = variant
+
+    def _run_pending(self):
+        pend = self.__dict__.get("_pending")
+        if not pend or pend[0] < 0:
+            return None
+        self._pending = [-1, 0, None]
+        flags, variant = pend[1], pend[2]
+        cur = getattr(self._cfg, "collide_variant", TWO_PHASE)
+        if variant is not None and variant != cur:
+            self._check(self._lib.dem_set_collide_variant(self._ctx, int(variant)))
+        m = _capi.dem_step_metrics()
+        try:
+            self._check(self._lib.dem_force_phase(self._ctx, flags, C.byref(m)))
+        finally:
+            if variant is not None and variant != cur:
+                self._lib.dem_set_collide_variant(self._ctx, int(cur))
+        self._last_composed = StepMetrics.from_c(m)
+        return self._last_composed
+
+    def kernel_integrate(self): self._compose("integrate")
+    def kernel_calc_hash(self): self._compose("calc_hash")
+    def kernel_bitonic_sort(self): self._compose("bitonic_sort")
+    def kernel_find_cell_bounds_and_reorder(self): self._compose("find_cell_bounds_and_reorder")
+    def zero_forces(self): self._compose("zero_forces")
+    def kernel_force_gravity(self): self._compose("force_gravity")
+    def kernel_initialize_contact_ids(self): self._compose("initialize_contact_ids")
+    def kernel_collide(self, variant: int = TWO_PHASE, record_traces: bool = False):
+        self._compose("collide", variant)
+    def kernel_collide_rectangle(self): self._compose("collide_rectangle")
+    def kernel_collide_line(self): self._compose("collide_line")
+
     # --- pipeline.hpp:64-86 ---
     def step(self) -> StepMetrics:
+        self._run_pending()
         m = _capi.dem_step_metrics()
         self._check(self._lib.dem_step(self._ctx, 1, C.byref(m)))
         return StepMetrics.from_c(m)
 
     def steps(self, n: int) -> StepMetrics:
+        self._run_pending()
         m = _capi.dem_step_metrics()
         self._check(self._lib.dem_step(self._ctx, n, C.byref(m)))
         return StepMetrics.from_c(m)
 
     def force_phase(self, flags: int) -> StepMetrics:
+        self._run_pending()
         m = _capi.dem_step_metrics()
         self._check(self._lib.dem_force_phase(self._ctx, flags, C.byref(m)))
         return StepMetrics.from_c(m)
@@ -387,15 +441,18 @@ class Simulation:
     def advance_and_collide(self) -> StepMetrics:
         """advance_to_collide + kernel_collide (tests/test_pipeline.cpp:69-76): integrate, bin,
         sweep, pp contacts only, no gravity, no walls."""
+        self._run_pending()
         return self.force_phase(_capi.PHASE_INTEGRATE | _capi.PHASE_PP)
 
     def set_record_traces(self, on: bool):
         self._record_traces = bool(on)  # traces are a §8f 'next' row; metrics are always on
 
     def set_collide_variant(self, v: int):
+        self._run_pending()
         self._check(self._lib.dem_set_collide_variant(self._ctx, int(v)))
 
     def clone(self) -> "Simulation":
+        self._run_pending()
         out = C.c_void_p()
         self._check(self._lib.dem_clone(self._ctx, C.byref(out)))
         s = Simulation(None, self._cfg, _ctx=out)
@@ -415,6 +472,7 @@ class Simulation:
         return int(self._lib.dem_step_index(self._ctx))
 
     def particles(self) -> ParticleSet:
+        self._run_pending()
         s = ParticleSet(self.size())
         self._check(self._lib.dem_get_particles(self._ctx, C.byref(s.c_struct())))
         return s
@@ -425,10 +483,12 @@ class Simulation:
         return s
 
     def set_particles(self, s: ParticleSet):
+        self._run_pending()
         s = s.contiguous()
         self._check(self._lib.dem_set_particles(self._ctx, C.byref(s.c_struct())))
 
     def forces(self) -> ForceAccumulator:
+        self._run_pending()
         n = self.size()
         f = np.zeros((n, 3))
         t = np.zeros((n, 3))
@@ -437,6 +497,7 @@ class Simulation:
         return ForceAccumulator(f, t)
 
     def set_forces(self, fa: ForceAccumulator):
+        self._run_pending()
         f = np.ascontiguousarray(fa.force, np.float64)
         t = np.ascontiguousarray(fa.torque, np.float64)
         self._check(self._lib.dem_set_forces(self._ctx, f.ctypes.data_as(C.POINTER(C.c_double)),
@@ -444,17 +505,20 @@ class Simulation:
 
     def periodic_box(self):
         """(cell extent per axis, Lees-Edwards image offset) — DESIGN.md §6."""
+        self._run_pending()
         ext = (C.c_double * 3)()
         off = C.c_double()
         self._check(self._lib.dem_get_periodic_box(self._ctx, ext, C.byref(off)))
         return tuple(ext), off.value
 
     def grid(self) -> Grid:
+        self._run_pending()
         g = _capi.dem_grid()
         self._check(self._lib.dem_get_grid(self._ctx, C.byref(g)))
         return Grid(tuple(g.origin), g.cell_size, g.nx, g.ny, g.nz)
 
     def order(self):
+        self._run_pending()
         n = self.size()
         k = np.zeros(n, np.uint32)
         p = np.zeros(n, np.uint32)
@@ -480,6 +544,7 @@ class Simulation:
     def traces(self):
         """Traversal traces of the last force phase (pipeline.hpp:97): (offsets[n+1] uint64,
         candidate slot int32[], contact bool[]); slot i's events are [offsets[i], offsets[i+1])."""
+        self._run_pending()
         n = self.size()
         off = np.zeros(n + 1, np.uint64)
         total = self._lib.dem_get_traces(self._ctx, off.ctypes.data_as(C.POINTER(C.c_uint64)), None, 0)
@@ -502,12 +567,14 @@ class Simulation:
 
     # --- measurement helpers (bench.py) ---
     def time_steps(self, nsteps: int, flush_bytes: int = 0):
+        self._run_pending()
         ms = (C.c_float * max(nsteps, 1))()
         m = _capi.dem_step_metrics()
         self._check(self._lib.dem_time_steps(self._ctx, nsteps, flush_bytes, ms, C.byref(m)))
         return [float(ms[k]) for k in range(nsteps)], StepMetrics.from_c(m)
 
     def profile_step(self, flush_bytes: int = 0) -> StepMetrics:
+        self._run_pending()
         m = _capi.dem_step_metrics()
         self._check(self._lib.dem_profile_step(self._ctx, flush_bytes, C.byref(m)))
         return StepMetrics.from_c(m)

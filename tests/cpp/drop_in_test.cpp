@@ -153,6 +153,43 @@ int main() {
         try { b2::Simulation s(s27, c); s.step(); } catch (const b2::CapacityError& e) { cap = e.kernel() == "Collide"; }
         EXPECT(cap);
     }
+    // the reference's per-kernel API (pipeline.hpp:77-86) composed as in tests/test_pipeline.cpp
+    // advance_to_collide + kernel_collide / walls: the same code drives both implementations
+    {
+        auto advance = [](auto& sim) {
+            sim.kernel_integrate();
+            sim.kernel_calc_hash();
+            sim.kernel_bitonic_sort();
+            sim.kernel_find_cell_bounds_and_reorder();
+            sim.zero_forces();
+            sim.kernel_initialize_contact_ids();
+        };
+        ref::Simulation ra(rs, rcfg);
+        b2::Simulation ba(bs, bcfg);
+        b2::Simulation bb(bs, bcfg);
+        for (int r = 0; r < 3; ++r) {
+            advance(ra);
+            advance(ba);
+            ra.kernel_collide(ref::CollideVariant::baseline, false);
+            ba.kernel_collide(b2::CollideVariant::baseline, false);
+            bb.force_phase(DEM_PHASE_INTEGRATE | DEM_PHASE_PP);
+        }
+        // composed kernels == the fused force phase, bitwise; and the reference to 1e-9
+        EXPECT(ba.particles() == bb.particles());
+        bool same_f = true;
+        for (std::size_t k = 0; k < n; ++k)
+            same_f = same_f && std::memcmp(&ba.forces().force[k], &bb.forces().force[k], sizeof(b2::Vec3)) == 0;
+        EXPECT(same_f);
+        std::map<std::uint32_t, std::size_t> ra_i, ba_i;
+        for (std::size_t k = 0; k < n; ++k) { ra_i[ra.particles().ids[k]] = k; ba_i[ba.particles().ids[k]] = k; }
+        double dfa = 0, fma = 0;
+        for (std::uint32_t id = 0; id < n; ++id) {
+            dfa = std::max(dfa, std::abs(ra.forces().force[ra_i[id]].x - ba.forces().force[ba_i[id]].x));
+            fma = std::max(fma, std::abs(ra.forces().force[ra_i[id]].x));
+        }
+        EXPECT(fma > 0 && dfa <= 1e-9 * fma);
+        EXPECT(ra.mean_coordination() == ba.mean_coordination());
+    }
     // configuration errors surface as ConfigError before any device work
     {
         auto c = basic_config<b2::SimConfig, b2::MaterialParams>(box);

@@ -206,3 +206,41 @@ def test_single_loop_variant_bitwise_equals_two_phase(cuda, seed):
     ha, _ = hist_from_gpu(a)
     hb, _ = hist_from_gpu(b)
     assert ha == hb
+
+
+def test_per_kernel_composition_equals_force_phase(cuda, orc):
+    """The reference's per-kernel API (pipeline.hpp:77-86) composed as tests/test_pipeline.cpp
+    advance_to_collide + kernel_collide / kernel_collide_rectangle / kernel_collide_line does:
+    bitwise equal to the fused phase, and to the C restatement's phase with the same flags."""
+    from oracle.oracle import OracleSim
+    dem = cuda
+    cfg = walled_config()
+    st = settling_state(300, 17)
+    a = dem.Simulation(st, cfg)
+    b = dem.Simulation(st, cfg)
+    o = OracleSim(orc, st, cfg)
+    for rnd in range(4):
+        a.kernel_integrate()
+        a.kernel_calc_hash()
+        a.kernel_bitonic_sort()
+        a.kernel_find_cell_bounds_and_reorder()
+        a.zero_forces()
+        a.kernel_force_gravity()
+        a.kernel_initialize_contact_ids()
+        a.kernel_collide(dem.BASELINE if rnd % 2 else dem.TWO_PHASE, False)
+        a.kernel_collide_rectangle()
+        a.kernel_collide_line()
+        b.force_phase(dem.PHASE_STEP)
+        o.force_phase(31)
+    pa, pb, po = a.particles(), b.particles(), o.state()
+    for fld in ("positions", "velocities", "angular_velocities"):
+        assert bitwise_equal(getattr(pa, fld), getattr(pb, fld)) and bitwise_equal(getattr(pa, fld), getattr(po, fld))
+    fa, fb = a.forces(), b.forces()
+    fo, to = o.forces()
+    assert bitwise_equal(fa.force, fb.force) and bitwise_equal(fa.force, fo) and bitwise_equal(fa.torque, to)
+    # a kernel earlier in pipeline order starts a new phase: integrate, then integrate again
+    a.kernel_integrate()
+    a.kernel_integrate()
+    b.force_phase(dem.PHASE_INTEGRATE)
+    b.force_phase(dem.PHASE_INTEGRATE)
+    assert bitwise_equal(a.particles().positions, b.particles().positions)

@@ -368,10 +368,13 @@ int build_graphs(dem_ctx* ctx) {
 }
 
 // Reads the control block after a sync; maps a device error to last_error.
-int collect(dem_ctx* ctx, dem_step_metrics* m, uint64_t phase_before, int64_t step_before, bool is_step) {
-    CUDA_TRY(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    CUDA_TRY(cudaGetLastError());
+int collect(dem_ctx* ctx, dem_step_metrics* m, uint64_t phase_before, int64_t step_before, bool is_step,
+            bool fetched = false) {
+    if (!fetched) {
+        CUDA_TRY(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        CUDA_TRY(cudaGetLastError());
+    }
     const DevCtl& d = *ctx->h_ctl;
     if (d.err_key != kNoError) {
         const uint64_t fail_phase = d.err_phase;
@@ -1133,8 +1136,12 @@ int dem_slab_migrate(dem_ctx* ctx, int integrate, void* send_lo, void* send_hi, 
     CUDA_TRY(cudaMemsetAsync(ctx->counters, 0, 8 * sizeof(uint32_t), ctx->stream));
     const StepParams p = make_params(ctx, 0);
     launch_slab_migrate(p, make_slab(ctx, send_lo, send_hi, cap_records), integrate != 0, ctx->stream);
-    int rc = read_counters(ctx);
-    if (rc == DEM_OK) rc = collect(ctx, nullptr, ctx->phase_count, ctx->step_index, false);
+    // one synchronisation for the record counts and the error word
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_counters, ctx->counters, 8 * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(ctx->h_ctl, ctx->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    CUDA_TRY(cudaGetLastError());
+    const int rc = collect(ctx, nullptr, ctx->phase_count, ctx->step_index, false, true);
     if (rc != DEM_OK) return rc;
     if (ctx->h_counters[4]) return set_error(ctx, DEM_ERR_CAPACITY, -1, 0, 0, ctx->step_index, "slab: migrant send buffer too small");
     ctx->n_own = ctx->h_counters[0];
@@ -1159,8 +1166,7 @@ int dem_slab_import(dem_ctx* ctx, const void* recs_lo, uint64_t n_lo, const void
     ctx->n_own += n_hi;
     ctx->imp_used += n_hi * ctx->K;
     ctx->n_asm = ctx->n_own;
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaGetLastError());  // stream-ordered: dem_slab_halo follows on the same stream
     return DEM_OK;
 }
 
@@ -1187,8 +1193,7 @@ int dem_slab_ghosts(dem_ctx* ctx, const void* recs_lo, uint64_t n_lo, const void
     launch_slab_ghosts(s, recs_lo, static_cast<uint32_t>(n_lo), static_cast<uint32_t>(ctx->n_own), false, ctx->stream);
     launch_slab_ghosts(s, recs_hi, static_cast<uint32_t>(n_hi), static_cast<uint32_t>(ctx->n_own + n_lo), true, ctx->stream);
     ctx->n_asm = ctx->n_own + n_lo + n_hi;
-    CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaGetLastError());  // stream-ordered: dem_slab_force follows on the same stream
     return DEM_OK;
 }
 

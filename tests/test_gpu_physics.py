@@ -67,6 +67,37 @@ def test_polydisperse_friction_bitwise(cuda, orc):
     assert m.capped_contacts > 0 and m.friction_max_ratio <= 1.0 + 1e-9
 
 
+def test_fullsize_config3_polydisperse_friction_bitwise(cuda, orc):
+    """BASELINE configs[2] at full size: 1,048,576 polydisperse spheres (radius ratio 1:2), sliding
+    friction active (omega ~ U(-50, 50)), K = 32; forces, torques, histories and pair sets
+    bitwise after two steps."""
+    dem = cuda
+    ps, dmax = dem.gen_packing(1048576, s=1.4, jit=0.2, poly=True, seed=3, omega_half=50.0)
+    sim, m = check_step_against_oracle(dem, orc, ps, dem.packing_config(dmax, poly=True), steps=2)
+    assert m.capped_contacts > 0.1 * m.contacts and m.friction_max_ratio <= 1.0 + 1e-9
+
+
+def test_config4_periodic_lees_edwards_1m_bitwise(cuda, orc):
+    """BASELINE configs[3] physics (fully periodic box, Lees-Edwards shear) at 1,048,576 spheres:
+    whole steps bitwise against the CPU restatement."""
+    from oracle.oracle import OracleSim
+    dem = cuda
+    ps, L = dem.gen_periodic_packing(1048576, s=1.8, jit=0.2, seed=4)
+    cfg = dem.periodic_config(L, shear_rate=1.0)
+    sim = dem.Simulation(ps, cfg)
+    osim = OracleSim(orc, ps, cfg)
+    for _ in range(2):
+        m = sim.step()
+        om = osim.step()
+        assert (m.contacts, m.pp_contact_events) == (om.contacts, om.pp_contact_events)
+    a, b = sim.particles(), osim.state()
+    assert np.array_equal(a.ids, b.ids)
+    assert bitwise_equal(a.positions, b.positions) and bitwise_equal(a.velocities, b.velocities)
+    fa = sim.forces()
+    fb, tb = osim.forces()
+    assert bitwise_equal(fa.force, fb) and bitwise_equal(fa.torque, tb)
+
+
 @pytest.mark.parametrize("s", [2.35, 2.2, 2.0, 1.6])
 def test_density_sweep_pair_sets(cuda, orc, s):
     """configs[4] packing-fraction sweep shape at 32,768 particles: exact pair sets at each s."""

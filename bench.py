@@ -215,17 +215,26 @@ def run_reference(args):
 
 def run_slab(args, world, rank, local):
     """N > 1: one packing of 262,144 x N spheres, cut into N z-slabs (weak scaling), one slab
-    per GPU, neighbour migrant/halo exchange over NCCL (paper_1503_03553_b200.slab)."""
+    per GPU; neighbour migrant/halo records stored into the neighbours' memory by the pack
+    kernels (CUDA IPC over NVLink), counts over gloo (paper_1503_03553_b200.slab.PeerTransport)."""
     import torch
     import torch.distributed as dist
     import paper_1503_03553_b200 as dem
-    from paper_1503_03553_b200.slab import SlabDriver, TorchTransport, build_local_slabs
+    from paper_1503_03553_b200.slab import PeerTransport, SlabDriver, TorchTransport, build_local_slabs
     n_total = N_PARTICLES * world
     ps, dmax = dem.gen_packing(n_total, s=1.8, jit=0.2, poly=False, seed=1)
     cfg = dem.packing_config(dmax)
     ranks, bounds, g = build_local_slabs(ps, cfg, world, [rank], device=local)
-    tr = TorchTransport(rank, world)
-    tr.bind(ranks[0])
+    # records through NVLink peer memory (pack kernels store into the neighbours' buffers); NCCL
+    # point-to-point messages if IPC peer access is unavailable on this box
+    transport = "peer"
+    try:
+        tr = PeerTransport(rank, world)
+        tr.bind(ranks[0])
+    except Exception:  # noqa: BLE001
+        transport = "nccl"
+        tr = TorchTransport(rank, world)
+        tr.bind(ranks[0])
     drv = SlabDriver(ranks, tr)
     drv.prime()
     for _ in range(args.warmup):
@@ -268,7 +277,8 @@ def run_slab(args, world, rank, local):
         "config": {"workload": f"{n_total:,} monodisperse spheres, dense packing = configs[1] per GPU",
                    "generator": f"G({n_total}, s=1.8, jit=0.2, mono, seed=1)", "dt": 1e-5,
                    "contact_capacity": 16, "contacts_per_step": int(c_all.item()),
-                   "parallelism": f"z-slabs x{world}, NCCL P2P halo + migration",
+                   "parallelism": f"z-slabs x{world}, halo + migration via "
+                                  + ("NVLink peer-memory stores (CUDA IPC)" if transport == "peer" else "NCCL P2P"),
                    "slabs": bounds, "l2": "flushed before every timed step, outside the events"},
         "gpu_launches": 11 * args.steps,
         "e2e": {"value": n_total * len(t_e2e) / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 0,

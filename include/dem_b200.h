@@ -275,6 +275,17 @@ int dem_slab_halo(dem_ctx* ctx, void* send_lo, void* send_hi, uint64_t cap_recor
 int dem_slab_ghosts(dem_ctx* ctx, const void* recs_lo, uint64_t n_lo, const void* recs_hi, uint64_t n_hi);
 int dem_slab_force(dem_ctx* ctx, uint32_t flags, dem_step_metrics* metrics);
 
+/* Peer-memory record exchange (one process per GPU, NVLink P2P): a rank allocates its receive
+ * buffers here, shares them with its z-neighbours as CUDA IPC handles (64 bytes each), and passes
+ * the neighbours' opened buffers as dem_slab_migrate / dem_slab_halo send buffers — the pack
+ * kernels then store the records straight into the neighbour's memory over NVLink, and only the
+ * record counts travel through the host. */
+int dem_ipc_alloc(int device, uint64_t bytes, void** ptr);
+int dem_ipc_free(int device, void* ptr);
+int dem_ipc_handle(int device, void* ptr, void* handle64);
+int dem_ipc_open(int device, const void* handle64, void** ptr);
+int dem_ipc_close(int device, void* ptr);
+
 #ifdef __cplusplus
 }
 #endif

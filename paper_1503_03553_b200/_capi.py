@@ -120,6 +120,11 @@ SIGNATURES = [
     ("dem_slab_halo", C.c_int, [_P, _P, _P, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     ("dem_slab_ghosts", C.c_int, [_P, _P, C.c_uint64, _P, C.c_uint64]),
     ("dem_slab_force", C.c_int, [_P, C.c_uint32, C.POINTER(dem_step_metrics)]),
+    ("dem_ipc_alloc", C.c_int, [C.c_int, C.c_uint64, C.POINTER(C.c_void_p)]),
+    ("dem_ipc_free", C.c_int, [C.c_int, C.c_void_p]),
+    ("dem_ipc_handle", C.c_int, [C.c_int, C.c_void_p, C.c_void_p]),
+    ("dem_ipc_open", C.c_int, [C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]),
+    ("dem_ipc_close", C.c_int, [C.c_int, C.c_void_p]),
 ]
 
 

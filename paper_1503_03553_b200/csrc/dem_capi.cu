@@ -1214,4 +1214,34 @@ int dem_slab_force(dem_ctx* ctx, uint32_t flags, dem_step_metrics* m) {
     return DEM_OK;
 }
 
+int dem_ipc_alloc(int device, uint64_t bytes, void** ptr) {
+    if (!ptr) return DEM_ERR_ARGUMENT;
+    if (cudaSetDevice(device) != cudaSuccess || cudaMalloc(ptr, bytes ? bytes : 16) != cudaSuccess) return DEM_ERR_CUDA;
+    return DEM_OK;
+}
+int dem_ipc_free(int device, void* ptr) {
+    if (cudaSetDevice(device) != cudaSuccess) return DEM_ERR_CUDA;
+    return cudaFree(ptr) == cudaSuccess ? DEM_OK : DEM_ERR_CUDA;
+}
+int dem_ipc_handle(int device, void* ptr, void* handle64) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handles are 64 bytes");
+    if (!ptr || !handle64) return DEM_ERR_ARGUMENT;
+    if (cudaSetDevice(device) != cudaSuccess) return DEM_ERR_CUDA;
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, ptr) != cudaSuccess) return DEM_ERR_CUDA;
+    std::memcpy(handle64, &h, sizeof(h));
+    return DEM_OK;
+}
+int dem_ipc_open(int device, const void* handle64, void** ptr) {
+    if (!handle64 || !ptr) return DEM_ERR_ARGUMENT;
+    if (cudaSetDevice(device) != cudaSuccess) return DEM_ERR_CUDA;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof(h));
+    return cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess ? DEM_OK : DEM_ERR_CUDA;
+}
+int dem_ipc_close(int device, void* ptr) {
+    if (cudaSetDevice(device) != cudaSuccess) return DEM_ERR_CUDA;
+    return cudaIpcCloseMemHandle(ptr) == cudaSuccess ? DEM_OK : DEM_ERR_CUDA;
+}
+
 }  // extern "C"

@@ -179,6 +179,84 @@ class TorchTransport:
         rk.recv_count[kind] = [m_lo, m_hi]
 
 
+class PeerTransport:
+    """One rank per process, records moved over NVLink peer memory instead of NCCL messages: each
+    rank's receive buffers are CUDA-IPC-shared with its z-neighbours, whose migrate / halo pack
+    kernels store the records straight into them (the pack and the transfer are one kernel).
+    Only the record counts travel, as one all-gather on a gloo group, which also orders the
+    neighbours' completed stores before this rank's unpack kernels. ring: periodic z."""
+
+    def __init__(self, rank: int, world: int, ring: bool = False):
+        import torch.distributed as dist
+        self.dist = dist
+        self.rank, self.world, self.ring = rank, world, ring
+        self.ctrl = dist.new_group(backend="gloo")
+        self.ranks = None
+        self.opened = []
+
+    def _nbr(self):
+        R, r = self.world, self.rank
+        lo = (r - 1) % R if (self.ring or r > 0) else None
+        hi = (r + 1) % R if (self.ring or r < R - 1) else None
+        return lo, hi
+
+    def bind(self, rk):
+        lib = _capi.lib()
+        self.ranks, self.lib, self.dev = [rk], lib, rk.device
+        rk.peer_recv, handles = {}, {}
+        for kind in ("migrant", "ghost"):
+            rk.peer_recv[kind], handles[kind] = [], []
+            for side in (0, 1):
+                ptr = C.c_void_p()
+                rc = lib.dem_ipc_alloc(self.dev, rk.cap[kind] * rk.rec_bytes[kind], C.byref(ptr))
+                if rc != 0:
+                    raise RuntimeError("dem_ipc_alloc failed")
+                h = (C.c_char * 64)()
+                if lib.dem_ipc_handle(self.dev, ptr, h) != 0:
+                    raise RuntimeError("dem_ipc_handle failed")
+                rk.peer_recv[kind].append(ptr.value)
+                handles[kind].append(bytes(h))
+        allh = [None] * self.world
+        self.dist.all_gather_object(allh, handles, group=self.ctrl)
+        lo, hi = self._nbr()
+        rk.peer_send = {}
+        for kind in ("migrant", "ghost"):
+            rk.peer_send[kind] = [None, None]
+            # my lo-side records land in the lower neighbour's "from above" buffer, and vice versa
+            for side, nbr, their_side in ((0, lo, 1), (1, hi, 0)):
+                if nbr is None:
+                    continue
+                if nbr == self.rank:
+                    rk.peer_send[kind][side] = rk.peer_recv[kind][their_side]
+                    continue
+                ptr = C.c_void_p()
+                if lib.dem_ipc_open(self.dev, (C.c_char * 64).from_buffer_copy(allh[nbr][kind][their_side]), C.byref(ptr)) != 0:
+                    raise RuntimeError("dem_ipc_open failed (no peer access to rank %d?)" % nbr)
+                rk.peer_send[kind][side] = ptr.value
+                self.opened.append(ptr.value)
+
+    def exchange(self, kind: str):
+        import torch
+        rk = self.ranks[0]
+        mine = torch.tensor(rk.send_count[kind], dtype=torch.int64)
+        allc = [torch.zeros(2, dtype=torch.int64) for _ in range(self.world)]
+        self.dist.all_gather(allc, mine, group=self.ctrl)
+        lo, hi = self._nbr()
+        rk.recv_count[kind] = [int(allc[lo][1]) if lo is not None else 0,
+                               int(allc[hi][0]) if hi is not None else 0]
+
+    def close(self):
+        for p in self.opened:
+            self.lib.dem_ipc_close(self.dev, C.c_void_p(p))
+        self.opened = []
+        rk = self.ranks[0] if self.ranks else None
+        if rk is not None and getattr(rk, "peer_recv", None):
+            for kind in rk.peer_recv:
+                for p in rk.peer_recv[kind]:
+                    self.lib.dem_ipc_free(self.dev, C.c_void_p(p))
+            rk.peer_recv, rk.peer_send = None, None
+
+
 # ---------------------------------------------------------------------------------------------
 # The CUDA-backed rank
 
@@ -226,6 +304,16 @@ class SlabRankCuda:
     def buffer_device(self):
         return self.send["migrant"][0].device
 
+    # device pointers the pack / unpack kernels use: this rank's torch buffers, or — under
+    # PeerTransport — the neighbours' receive buffers (send) and IPC-shareable ones (receive)
+    def send_ptr(self, kind, side):
+        o = getattr(self, "peer_send", None)
+        return o[kind][side] if o and o[kind][side] else self.send[kind][side].data_ptr()
+
+    def recv_ptr(self, kind, side):
+        o = getattr(self, "peer_recv", None)
+        return o[kind][side] if o else self.recv[kind][side].data_ptr()
+
     def send_view(self, kind, side, n):
         return self.send[kind][side][: n * self.rec_bytes[kind]]
 
@@ -239,28 +327,28 @@ class SlabRankCuda:
     # --- phases ---
     def migrate(self, integrate: bool):
         lo, hi = C.c_uint64(), C.c_uint64()
-        self._check(self.lib.dem_slab_migrate(self.ctx, 1 if integrate else 0, self.send["migrant"][0].data_ptr(),
-                                              self.send["migrant"][1].data_ptr(), self.cap["migrant"],
+        self._check(self.lib.dem_slab_migrate(self.ctx, 1 if integrate else 0, self.send_ptr("migrant", 0),
+                                              self.send_ptr("migrant", 1), self.cap["migrant"],
                                               C.byref(lo), C.byref(hi)))
         self.send_count["migrant"] = [lo.value, hi.value]
 
     def import_(self):
         self.torch.cuda.synchronize(self.device)
         n_lo, n_hi = self.recv_count["migrant"]
-        self._check(self.lib.dem_slab_import(self.ctx, self.recv["migrant"][0].data_ptr(), n_lo,
-                                             self.recv["migrant"][1].data_ptr(), n_hi))
+        self._check(self.lib.dem_slab_import(self.ctx, self.recv_ptr("migrant", 0), n_lo,
+                                             self.recv_ptr("migrant", 1), n_hi))
 
     def halo(self):
         lo, hi = C.c_uint64(), C.c_uint64()
-        self._check(self.lib.dem_slab_halo(self.ctx, self.send["ghost"][0].data_ptr(), self.send["ghost"][1].data_ptr(),
+        self._check(self.lib.dem_slab_halo(self.ctx, self.send_ptr("ghost", 0), self.send_ptr("ghost", 1),
                                            self.cap["ghost"], C.byref(lo), C.byref(hi)))
         self.send_count["ghost"] = [lo.value, hi.value]
 
     def ghosts(self):
         self.torch.cuda.synchronize(self.device)
         n_lo, n_hi = self.recv_count["ghost"]
-        self._check(self.lib.dem_slab_ghosts(self.ctx, self.recv["ghost"][0].data_ptr(), n_lo,
-                                             self.recv["ghost"][1].data_ptr(), n_hi))
+        self._check(self.lib.dem_slab_ghosts(self.ctx, self.recv_ptr("ghost", 0), n_lo,
+                                             self.recv_ptr("ghost", 1), n_hi))
 
     def force(self, flags: int) -> StepMetrics:
         m = _capi.dem_step_metrics()

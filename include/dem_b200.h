@@ -192,6 +192,15 @@ void dem_destroy(dem_ctx* ctx);
  * receives the last step's metrics. Stops at the first failing step. */
 int dem_step(dem_ctx* ctx, int nsteps, dem_step_metrics* last);
 
+/* Asynchronous stepping for host-coupled callers (B200 addition): enqueue nsteps and return at
+ * once. The next call that reads or replaces the state collects them — an error of an
+ * asynchronous step is reported there, attributed to the failing step — and dem_sync collects
+ * explicitly, returning the last step's metrics. dem_get_particles right after dem_step_async
+ * reads the state back while the last step's detection and forces still run (its state is final
+ * after the reorder), then waits for the step. Not for slab contexts. */
+int dem_step_async(dem_ctx* ctx, int nsteps);
+int dem_sync(dem_ctx* ctx, dem_step_metrics* last);
+
 /* A composed force phase (flags, see dem_phase_flags). DEM_PHASE_STEP == step(). */
 int dem_force_phase(dem_ctx* ctx, uint32_t flags, dem_step_metrics* metrics);
 
@@ -285,6 +294,11 @@ int dem_ipc_free(int device, void* ptr);
 int dem_ipc_handle(int device, void* ptr, void* handle64);
 int dem_ipc_open(int device, const void* handle64, void** ptr);
 int dem_ipc_close(int device, void* ptr);
+
+/* Diagnostics: the force kernel's shared-reciprocal division against the plain IEEE '/' on n
+ * seeded random operand pairs (random bit patterns, exponents around the
+ * fast-path bounds, contact-like magnitudes). *mismatches = results that differ in any bit. */
+int dem_selftest_division(int device, uint64_t n, uint64_t seed, uint64_t* mismatches);
 
 #ifdef __cplusplus
 }

@@ -86,6 +86,8 @@ SIGNATURES = [
     ("dem_clone", C.c_int, [_P, C.POINTER(_P)]),
     ("dem_destroy", None, [_P]),
     ("dem_step", C.c_int, [_P, C.c_int, C.POINTER(dem_step_metrics)]),
+    ("dem_step_async", C.c_int, [_P, C.c_int]),
+    ("dem_sync", C.c_int, [_P, C.POINTER(dem_step_metrics)]),
     ("dem_force_phase", C.c_int, [_P, C.c_uint32, C.POINTER(dem_step_metrics)]),
     ("dem_set_collide_variant", C.c_int, [_P, C.c_int]),
     ("dem_size", C.c_uint64, [_P]),
@@ -125,6 +127,7 @@ SIGNATURES = [
     ("dem_ipc_handle", C.c_int, [C.c_int, C.c_void_p, C.c_void_p]),
     ("dem_ipc_open", C.c_int, [C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]),
     ("dem_ipc_close", C.c_int, [C.c_int, C.c_void_p]),
+    ("dem_selftest_division", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64)]),
 ]
 
 

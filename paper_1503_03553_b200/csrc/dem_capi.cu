@@ -95,6 +95,15 @@ struct dem_ctx {
     size_t tile_pairs = 0, imp_cap = 0, imp_used = 0;
     uint32_t rec_bytes = 0, rec_dt_off = 0, ghost_bytes = 0;
 
+    // asynchronous stepping (dem_step_async): steps launched but not yet collected, and the
+    // readback stream that overlaps dem_get_particles with the tail of the last step
+    bool inflight = false;
+    uint64_t inflight_pb = 0;
+    int64_t inflight_sb = 0;
+    dem_step_metrics async_last{};
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_state[2] = {nullptr, nullptr};  // recorded by step graph [parity] after k_reorder
+
     // device staging in the host layout for get/set (allocated on first use)
     double* raw_d = nullptr;
     uint32_t* raw_u = nullptr;
@@ -326,7 +335,10 @@ PhaseBufs make_bufs(const dem_ctx* c, uint64_t phase) {
 }
 
 // Enqueue one force phase; with `ev` (9 events) records an event after each kernel.
-void enqueue_phase(const dem_ctx* c, uint32_t flags, uint64_t phase, cudaEvent_t* ev) {
+// state_ready (graphs only): an external event node after k_reorder — the phase's particle state
+// is final there (detection and forces only read it), so a readback can overlap them.
+void enqueue_phase(const dem_ctx* c, uint32_t flags, uint64_t phase, cudaEvent_t* ev,
+                   cudaEvent_t state_ready = nullptr) {
     const StepParams p = make_params(c, flags);
     const PhaseBufs b = make_bufs(c, phase);
     cudaStream_t s = c->stream;
@@ -341,6 +353,7 @@ void enqueue_phase(const dem_ctx* c, uint32_t flags, uint64_t phase, cudaEvent_t
     if (ev) cudaEventRecord(ev[4], s);
     launch_reorder(p, b, s);
     if (ev) cudaEventRecord(ev[5], s);
+    if (state_ready) cudaEventRecordWithFlags(state_ready, s, cudaEventRecordExternal);
     if (c->collide_variant == 0) {
         // Alg. 1, single loop (pipeline.cpp:209-217): detection and forces in one divergent loop
         launch_collide_single_loop(p, b, s);
@@ -358,8 +371,9 @@ int build_graphs(dem_ctx* ctx) {
     for (int par = 0; par < 2; ++par) {
         if (ctx->graph[par]) { cudaGraphExecDestroy(ctx->graph[par]); ctx->graph[par] = nullptr; }
         cudaGraph_t g;
+        if (!ctx->ev_state[par]) CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_state[par], cudaEventDisableTiming));
         CUDA_TRY(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-        enqueue_phase(ctx, DEM_PHASE_STEP, static_cast<uint64_t>(par), nullptr);
+        enqueue_phase(ctx, DEM_PHASE_STEP, static_cast<uint64_t>(par), nullptr, ctx->ev_state[par]);
         CUDA_TRY(cudaStreamEndCapture(ctx->stream, &g));
         CUDA_TRY(cudaGraphInstantiate(&ctx->graph[par], g, 0));
         cudaGraphDestroy(g);
@@ -421,10 +435,29 @@ int collect(dem_ctx* ctx, dem_step_metrics* m, uint64_t phase_before, int64_t st
     return DEM_OK;
 }
 
+// Collects steps launched by dem_step_async (sync, error mapping, metrics of the last one). Every
+// entry point that reads or replaces device state settles first, so an asynchronous step's error
+// surfaces at the next such call, attributed to the step that failed.
+int settle(dem_ctx* ctx) {
+    if (!ctx->inflight) return DEM_OK;
+    ctx->inflight = false;
+    std::memset(&ctx->async_last, 0, sizeof(ctx->async_last));
+    return collect(ctx, &ctx->async_last, ctx->inflight_pb, ctx->inflight_sb, true);
+}
+#define SETTLE(ctx)                                  \
+    do {                                             \
+        const int settle_rc_ = settle(ctx);          \
+        if (settle_rc_ != DEM_OK) return settle_rc_; \
+    } while (0)
+
 void free_ctx(dem_ctx* c) {
     if (!c) return;
     if (c->device >= 0) cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->side) cudaStreamSynchronize(c->side);
     for (auto& g : c->graph) if (g) cudaGraphExecDestroy(g);
+    for (auto& e : c->ev_state) if (e) cudaEventDestroy(e);
+    if (c->side) cudaStreamDestroy(c->side);
     for (void* p : c->allocations) cudaFree(p);
     if (c->flush_buf) cudaFree(c->flush_buf);
     if (c->h_ctl) cudaFreeHost(c->h_ctl);
@@ -561,6 +594,8 @@ int upload_state(dem_ctx* ctx, const dem_particles* p, int buf) {
     launch_pack_state(ctx->state[buf], r, static_cast<uint32_t>(n), true, s);
     // the monodisperse detection shortcut compares every radius with this one (k_integrate_hash)
     CUDA_TRY(cudaMemcpyAsync(&ctx->ctl->r_ref, p->radii, sizeof(double), cudaMemcpyHostToDevice, s));
+    // k_force_reduce memoises r_eff, m_eff, k_n for contacts of two particles equal to these
+    CUDA_TRY(cudaMemcpyAsync(&ctx->ctl->m_ref, p->masses, sizeof(double), cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     CUDA_TRY(cudaGetLastError());
     return DEM_OK;
@@ -670,6 +705,8 @@ int dem_create(const dem_config* cfg, const dem_particles* particles, int device
 
 int dem_clone(const dem_ctx* src, dem_ctx** out) {
     if (!src || !out || src->slab) return DEM_ERR_ARGUMENT;
+    cudaSetDevice(src->device);
+    SETTLE(const_cast<dem_ctx*>(src));
     dem_ctx* ctx = new (std::nothrow) dem_ctx();
     if (!ctx) return DEM_ERR_ARGUMENT;
     ctx->device = src->device;
@@ -734,6 +771,7 @@ void dem_destroy(dem_ctx* ctx) { free_ctx(ctx); }
 int dem_step(dem_ctx* ctx, int nsteps, dem_step_metrics* last) {
     if (!ctx || nsteps < 0) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
+    SETTLE(ctx);
     if (ctx->n == 0) {
         ctx->step_index += nsteps;
         if (last) { std::memset(last, 0, sizeof(*last)); last->step = ctx->step_index; }
@@ -749,9 +787,38 @@ int dem_step(dem_ctx* ctx, int nsteps, dem_step_metrics* last) {
     return collect(ctx, last, pb, sb, true);
 }
 
+int dem_step_async(dem_ctx* ctx, int nsteps) {
+    if (!ctx || nsteps < 0 || ctx->slab) return DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    if (ctx->n == 0) {
+        ctx->step_index += nsteps;
+        return DEM_OK;
+    }
+    if (!ctx->inflight) {
+        ctx->inflight = true;
+        ctx->inflight_pb = ctx->phase_count;
+        ctx->inflight_sb = ctx->step_index;
+    }
+    for (int k = 0; k < nsteps; ++k) {
+        ++ctx->phase_count;
+        ++ctx->step_index;
+        CUDA_TRY(cudaGraphLaunch(ctx->graph[ctx->phase_count & 1], ctx->stream));
+    }
+    return DEM_OK;
+}
+
+int dem_sync(dem_ctx* ctx, dem_step_metrics* last) {
+    if (!ctx) return DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    const int rc = settle(ctx);
+    if (last) *last = ctx->async_last;
+    return rc;
+}
+
 int dem_force_phase(dem_ctx* ctx, uint32_t flags, dem_step_metrics* m) {
     if (!ctx || (flags & ~static_cast<uint32_t>(DEM_PHASE_STEP))) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
+    SETTLE(ctx);
     return run_phase(ctx, flags, m, flags == DEM_PHASE_STEP);
 }
 
@@ -760,6 +827,8 @@ int dem_set_collide_variant(dem_ctx* ctx, int variant) {
     if ((ctx->periodic || ctx->precision) && variant == 0)
         return set_error(ctx, DEM_ERR_CONFIG, -1, 0, 0, ctx->step_index, "periodic boxes and the fp32 mode run the two_phase collide variant");
     if (ctx->collide_variant == variant) return DEM_OK;
+    cudaSetDevice(ctx->device);
+    SETTLE(ctx);
     ctx->collide_variant = variant;
     cudaSetDevice(ctx->device);
     return ctx->slab ? DEM_OK : build_graphs(ctx);  // step graphs embed the Collide kernels
@@ -774,11 +843,21 @@ int dem_get_particles(dem_ctx* ctx, dem_particles* out) {
     if (!ctx || !out || out->count != ctx->n) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
     const uint64_t n = ctx->n;
-    if (!n) return DEM_OK;
+    if (!n) return settle(ctx);
     int rc = ensure_raw(ctx, n);
     if (rc != DEM_OK) return rc;
     const RawState r = raw_view(ctx, n);
     cudaStream_t s = ctx->stream;
+    // After dem_step_async the last step's state is final once its k_reorder has run: the
+    // readback goes on the side stream from there and overlaps the step's detection and forces.
+    const bool overlap = ctx->inflight && !ctx->slab;
+    if (overlap) {
+        if (!ctx->side) CUDA_TRY(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+        s = ctx->side;
+        CUDA_TRY(cudaStreamWaitEvent(s, ctx->ev_state[ctx->phase_count & 1], 0));
+    } else {
+        SETTLE(ctx);
+    }
     launch_pack_state(ctx->state[state_cur(ctx)], r, static_cast<uint32_t>(n), false, s);
     if (out->positions) CUDA_TRY(cudaMemcpyAsync(out->positions, r.pos, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, s));
     if (out->velocities) CUDA_TRY(cudaMemcpyAsync(out->velocities, r.vel, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -787,9 +866,10 @@ int dem_get_particles(dem_ctx* ctx, dem_particles* out) {
     if (out->masses) CUDA_TRY(cudaMemcpyAsync(out->masses, r.mass, n * sizeof(double), cudaMemcpyDeviceToHost, s));
     if (out->ids) CUDA_TRY(cudaMemcpyAsync(out->ids, r.ids, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     if (out->material_ids) CUDA_TRY(cudaMemcpyAsync(out->material_ids, r.mat, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    rc = overlap ? settle(ctx) : DEM_OK;  // the step's own completion and error check
     CUDA_TRY(cudaStreamSynchronize(s));
     CUDA_TRY(cudaGetLastError());
-    return DEM_OK;
+    return rc;
 }
 
 int dem_set_particles(dem_ctx* ctx, const dem_particles* in) {
@@ -797,6 +877,7 @@ int dem_set_particles(dem_ctx* ctx, const dem_particles* in) {
     if (!in->ids || !in->positions || !in->velocities || !in->angular_velocities || !in->radii || !in->masses || !in->material_ids)
         return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
+    SETTLE(ctx);
     ctx->replaced_at = ctx->phase_count;  // the binning no longer matches the state (traces)
     return upload_state(ctx, in, state_cur(ctx));
 }
@@ -804,6 +885,7 @@ int dem_set_particles(dem_ctx* ctx, const dem_particles* in) {
 int dem_get_forces(dem_ctx* ctx, double* force, double* torque) {
     if (!ctx) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
+    SETTLE(ctx);
     const uint64_t n = ctx->n, fs = ft_stride(ctx);
     if (!n) return DEM_OK;
     int rc = ensure_raw(ctx, n);
@@ -821,6 +903,7 @@ int dem_get_forces(dem_ctx* ctx, double* force, double* torque) {
 int dem_set_forces(dem_ctx* ctx, const double* force, const double* torque) {
     if (!ctx || !force || !torque) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
+    SETTLE(ctx);
     const uint64_t n = ctx->n, fs = ft_stride(ctx);
     if (!n) return DEM_OK;
     int rc = ensure_raw(ctx, n);
@@ -843,6 +926,8 @@ int dem_get_grid(const dem_ctx* ctx, dem_grid* out) {
 
 int dem_get_periodic_box(dem_ctx* ctx, double cell_extent[3], double* shear_offset) {
     if (!ctx) return DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    SETTLE(ctx);
     if (cell_extent) for (int a = 0; a < 3; ++a) cell_extent[a] = ctx->cell_extent[a];
     if (shear_offset) {
         cudaSetDevice(ctx->device);
@@ -854,6 +939,7 @@ int dem_get_periodic_box(dem_ctx* ctx, double cell_extent[3], double* shear_offs
 int dem_get_order(dem_ctx* ctx, uint32_t* sorted_keys, uint32_t* permutation) {
     if (!ctx) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
+    SETTLE(ctx);
     const uint64_t n = ctx->n;
     if (n && sorted_keys) CUDA_TRY(cudaMemcpyAsync(sorted_keys, ctx->skey, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
     if (n && permutation) CUDA_TRY(cudaMemcpyAsync(permutation, ctx->prev_slot, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
@@ -864,6 +950,7 @@ int dem_get_order(dem_ctx* ctx, uint32_t* sorted_keys, uint32_t* permutation) {
 int64_t dem_get_contacts(dem_ctx* ctx, uint32_t* owner_slot, int32_t* partner, double* delta_t, int64_t cap) {
     if (!ctx) return -DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
+    if (const int rc_ = settle(ctx)) return -rc_;
     const uint64_t n = ctx->n;
     if (n == 0) return 0;
     const HistBuf& h = ctx->hist[hist_cur(ctx)];
@@ -891,6 +978,7 @@ int64_t dem_get_contacts(dem_ctx* ctx, uint32_t* owner_slot, int32_t* partner, d
 int64_t dem_get_traces(dem_ctx* ctx, uint64_t* offsets, dem_trace_event* events, int64_t capacity) {
     if (!ctx || ctx->slab || ctx->periodic || ctx->phase_count == 0 || ctx->replaced_at == ctx->phase_count) return -DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
+    if (const int rc_ = settle(ctx)) return -rc_;
     const uint64_t n = ctx->n;
     if (n == 0) {
         if (offsets) offsets[0] = 0;
@@ -943,6 +1031,7 @@ int dem_last_error(const dem_ctx* ctx, dem_error* out) {
 int dem_time_steps(dem_ctx* ctx, int nsteps, size_t flush_bytes, float* step_ms, dem_step_metrics* last) {
     if (!ctx || nsteps < 0 || (nsteps && !step_ms)) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
+    SETTLE(ctx);
     if (flush_bytes && flush_bytes != ctx->flush_bytes) {
         if (ctx->flush_buf) cudaFree(ctx->flush_buf);
         ctx->flush_buf = nullptr;
@@ -970,6 +1059,7 @@ int dem_time_steps(dem_ctx* ctx, int nsteps, size_t flush_bytes, float* step_ms,
 int dem_profile_step(dem_ctx* ctx, size_t flush_bytes, dem_step_metrics* m) {
     if (!ctx || !m) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
+    SETTLE(ctx);
     if (flush_bytes && flush_bytes != ctx->flush_bytes) {
         if (ctx->flush_buf) cudaFree(ctx->flush_buf);
         ctx->flush_buf = nullptr;
@@ -1242,6 +1332,23 @@ int dem_ipc_open(int device, const void* handle64, void** ptr) {
 int dem_ipc_close(int device, void* ptr) {
     if (cudaSetDevice(device) != cudaSuccess) return DEM_ERR_CUDA;
     return cudaIpcCloseMemHandle(ptr) == cudaSuccess ? DEM_OK : DEM_ERR_CUDA;
+}
+
+int dem_selftest_division(int device, uint64_t n, uint64_t seed, uint64_t* mismatches) {
+    if (!mismatches) return DEM_ERR_ARGUMENT;
+    if (cudaSetDevice(device) != cudaSuccess) return DEM_ERR_CUDA;
+    unsigned long long* d = nullptr;
+    if (cudaMalloc(&d, sizeof(*d)) != cudaSuccess) return DEM_ERR_CUDA;
+    unsigned long long h = 0;
+    cudaError_t e = cudaMemset(d, 0, sizeof(*d));
+    if (e == cudaSuccess) {
+        launch_selftest_division(n, seed, d, 0);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    *mismatches = h;
+    return e == cudaSuccess ? DEM_OK : DEM_ERR_CUDA;
 }
 
 }  // extern "C"

@@ -73,6 +73,7 @@ struct DevCtl {
     unsigned int odd_radius;                    // a radius outside [1e-100, 1e100] (or NaN) was binned
     unsigned int poly;                          // a radius != r_ref was binned this phase
     double r_ref;                               // a radius of the state (set on upload)
+    double m_ref;                               // a mass of the state (set on upload; force memo)
     long long le_steps;                         // integrating phases so far (Lees-Edwards clock)
     double le_delta;                            // Lees-Edwards image offset of the upper box
 };
@@ -164,6 +165,7 @@ void launch_force_reduce(const StepParams& p, const PhaseBufs& b, cudaStream_t s
 void launch_collide_single_loop(const StepParams& p, const PhaseBufs& b, cudaStream_t s);
 void launch_flush(void* buf, size_t bytes, cudaStream_t s);
 // traversal traces of the phase whose buffers `b` names (ev == nullptr: per-slot counts)
+void launch_selftest_division(uint64_t n, uint64_t seed, unsigned long long* bad, cudaStream_t s);
 void launch_trace(const StepParams& p, const PhaseBufs& b, const unsigned long long* off, int2* ev,
                   uint32_t* count, cudaStream_t s);
 

@@ -432,6 +432,19 @@ class Simulation:
         self._check(self._lib.dem_step(self._ctx, n, C.byref(m)))
         return StepMetrics.from_c(m)
 
+    def step_async(self, n: int = 1) -> None:
+        """Enqueue n steps and return at once (dem_step_async). The next call that reads or
+        replaces the state reports their errors; particles() / particles_into() right after it
+        overlap the readback with the last step's detection and forces."""
+        self._run_pending()
+        self._check(self._lib.dem_step_async(self._ctx, n))
+
+    def sync(self) -> StepMetrics:
+        """Wait for asynchronous steps; the last one's metrics (dem_sync)."""
+        m = _capi.dem_step_metrics()
+        self._check(self._lib.dem_sync(self._ctx, C.byref(m)))
+        return StepMetrics.from_c(m)
+
     def force_phase(self, flags: int) -> StepMetrics:
         self._run_pending()
         m = _capi.dem_step_metrics()

@@ -72,8 +72,8 @@ struct DevCtl {
     unsigned long long contacts;
     unsigned int odd_radius;                    // a radius outside [1e-100, 1e100] (or NaN) was binned
     unsigned int poly;                          // a radius != r_ref was binned this phase
-    double r_ref;                               // a radius of the state (set on upload)
-    double m_ref;                               // a mass of the state (set on upload; force memo)
+    double r_ref;                               // particle 0's radius (set on upload; k_pack_state)
+    double m_ref;                               // its mass (force memo); must follow r_ref
     long long le_steps;                         // integrating phases so far (Lees-Edwards clock)
     double le_delta;                            // Lees-Edwards image offset of the upper box
 };
@@ -174,7 +174,9 @@ struct RawState {
     double *pos, *vel, *omg, *rad, *mass;
     uint32_t *ids, *mat;
 };
-void launch_pack_state(const StateBuf& s, const RawState& r, uint32_t n, bool pack, cudaStream_t st);
+// pack: host layout -> SoA, and (ref non-null) ref[0], ref[1] = particle 0's radius and mass
+void launch_pack_state(const StateBuf& s, const RawState& r, uint32_t n, bool pack, cudaStream_t st,
+                       double* ref = nullptr);
 void launch_ft_layout(double* ft, uint32_t stride, double* f, double* t, uint32_t n, bool to_interleaved, cudaStream_t st);
 cudaError_t init_device_attributes();
 

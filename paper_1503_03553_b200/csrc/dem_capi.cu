@@ -74,6 +74,7 @@ struct dem_ctx {
     uint64_t replaced_at = ~0ull;  // phase_count when dem_set_particles last replaced the state
     int64_t step_index = 0;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    cudaGraphExec_t graph_async[2] = {nullptr, nullptr};  // + the state-ready event node (dem_step_async)
     void* flush_buf = nullptr;
     size_t flush_bytes = 0;
     DevCtl* h_ctl = nullptr;  // pinned readback
@@ -367,16 +368,21 @@ void enqueue_phase(const dem_ctx* c, uint32_t flags, uint64_t phase, cudaEvent_t
     }
 }
 
+// Step graphs per phase parity; the asynchronous ones also record ev_state after k_reorder (an
+// event node between kernels costs ~1 us of launch latency, so dem_step runs without it).
 int build_graphs(dem_ctx* ctx) {
     for (int par = 0; par < 2; ++par) {
-        if (ctx->graph[par]) { cudaGraphExecDestroy(ctx->graph[par]); ctx->graph[par] = nullptr; }
-        cudaGraph_t g;
         if (!ctx->ev_state[par]) CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_state[par], cudaEventDisableTiming));
-        CUDA_TRY(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-        enqueue_phase(ctx, DEM_PHASE_STEP, static_cast<uint64_t>(par), nullptr, ctx->ev_state[par]);
-        CUDA_TRY(cudaStreamEndCapture(ctx->stream, &g));
-        CUDA_TRY(cudaGraphInstantiate(&ctx->graph[par], g, 0));
-        cudaGraphDestroy(g);
+        for (int async = 0; async < 2; ++async) {
+            cudaGraphExec_t& ge = async ? ctx->graph_async[par] : ctx->graph[par];
+            if (ge) { cudaGraphExecDestroy(ge); ge = nullptr; }
+            cudaGraph_t g;
+            CUDA_TRY(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+            enqueue_phase(ctx, DEM_PHASE_STEP, static_cast<uint64_t>(par), nullptr, async ? ctx->ev_state[par] : nullptr);
+            CUDA_TRY(cudaStreamEndCapture(ctx->stream, &g));
+            CUDA_TRY(cudaGraphInstantiate(&ge, g, 0));
+            cudaGraphDestroy(g);
+        }
     }
     return DEM_OK;
 }
@@ -456,6 +462,7 @@ void free_ctx(dem_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->side) cudaStreamSynchronize(c->side);
     for (auto& g : c->graph) if (g) cudaGraphExecDestroy(g);
+    for (auto& g : c->graph_async) if (g) cudaGraphExecDestroy(g);
     for (auto& e : c->ev_state) if (e) cudaEventDestroy(e);
     if (c->side) cudaStreamDestroy(c->side);
     for (void* p : c->allocations) cudaFree(p);
@@ -803,7 +810,7 @@ int dem_step_async(dem_ctx* ctx, int nsteps) {
     for (int k = 0; k < nsteps; ++k) {
         ++ctx->phase_count;
         ++ctx->step_index;
-        CUDA_TRY(cudaGraphLaunch(ctx->graph[ctx->phase_count & 1], ctx->stream));
+        CUDA_TRY(cudaGraphLaunch(ctx->graph_async[ctx->phase_count & 1], ctx->stream));
     }
     return DEM_OK;
 }

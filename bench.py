@@ -370,6 +370,24 @@ def run_b200(args):
     e2e_s = max_over_ranks(sum(t_e2e), world)
     e2e_value = n * e2e_steps * world / e2e_s
     state_bytes = n * (4 + 24 * 3 + 8 + 8 + 4)
+    # the host-coupled variant: only the motion goes up (positions, velocities, angular velocities;
+    # ids / radii / masses / materials stay on the device), the motion and ids come back
+    motion = pinned_particles(n)
+    motion.radii = motion.masses = motion.material_ids = None
+    sim.particles_into(motion)
+    t_mo = []
+    for _ in range(e2e_steps):
+        t0 = time.perf_counter()
+        sim.set_motion(motion.positions, motion.velocities, motion.angular_velocities)
+        sim.step_async()
+        sim.particles_into(motion)
+        m_e2e = sim.sync()
+        t_mo.append(time.perf_counter() - t0)
+    mo_s = max_over_ranks(sum(t_mo), world)
+    e2e_motion = {"value": n * e2e_steps * world / mo_s, "unit": UNIT, "h2d_bytes_per_step": n * 72,
+                  "d2h_bytes_per_step": n * 76,
+                  "how": "dem_set_particles(motion only; ids/radii/masses/materials NULL = kept) + "
+                         "dem_step_async + dem_get_particles(motion + ids) + dem_sync, wall clock"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -385,6 +403,7 @@ def run_b200(args):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": state_bytes,
                 "d2h_bytes_per_step": state_bytes,
                 "how": "dem_set_particles(pinned host) + dem_step_async(1) + dem_get_particles(pinned host, overlapping the step's detection and forces) + dem_sync (metrics), wall clock"},
+        "e2e_motion": e2e_motion,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_ach, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": dom_ach / peak,
                      "traffic": traffic, "algorithmic_bytes": nbytes[dom], "ms": kms[dom],

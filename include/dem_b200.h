@@ -212,6 +212,10 @@ int dem_set_collide_variant(dem_ctx* ctx, int variant);
 uint64_t dem_size(const dem_ctx* ctx);
 int64_t dem_step_index(const dem_ctx* ctx);
 int dem_get_particles(dem_ctx* ctx, dem_particles* out);
+/* positions, velocities, angular_velocities are required; ids, radii, masses, material_ids may be
+ * NULL, in which case every slot keeps its current value (the given arrays are then in the current
+ * slot order, as dem_get_particles returns it) — a host-coupled caller that changes only the
+ * motion moves 72 of the 96 bytes per particle. In dem_get_particles any array may be NULL. */
 int dem_set_particles(dem_ctx* ctx, const dem_particles* in);
 int dem_get_forces(dem_ctx* ctx, double* force, double* torque);
 int dem_set_forces(dem_ctx* ctx, const double* force, const double* torque);

@@ -592,18 +592,24 @@ int upload_state(dem_ctx* ctx, const dem_particles* p, int buf) {
     cudaStream_t s = ctx->stream;
     int rc = ensure_raw(ctx, n);
     if (rc != DEM_OK) return rc;
-    const RawState r = raw_view(ctx, n);
+    RawState r = raw_view(ctx, n);
+    // ids, radii, masses, material ids may be NULL (dem_set_particles): the slots keep theirs
+    if (!p->radii) r.rad = nullptr;
+    if (!p->masses) r.mass = nullptr;
+    if (!p->ids) r.ids = nullptr;
+    if (!p->material_ids) r.mat = nullptr;
     CUDA_TRY(cudaMemcpyAsync(r.pos, p->positions, 3 * n * sizeof(double), cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(r.vel, p->velocities, 3 * n * sizeof(double), cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(r.omg, p->angular_velocities, 3 * n * sizeof(double), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(r.rad, p->radii, n * sizeof(double), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(r.mass, p->masses, n * sizeof(double), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(r.ids, p->ids, n * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(r.mat, p->material_ids, n * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    if (r.rad) CUDA_TRY(cudaMemcpyAsync(r.rad, p->radii, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (r.mass) CUDA_TRY(cudaMemcpyAsync(r.mass, p->masses, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (r.ids) CUDA_TRY(cudaMemcpyAsync(r.ids, p->ids, n * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    if (r.mat) CUDA_TRY(cudaMemcpyAsync(r.mat, p->material_ids, n * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
     // + r_ref, m_ref = particle 0's radius and mass: the monodisperse detection shortcut compares
     // every radius with r_ref (k_integrate_hash); k_force_reduce memoises r_eff, m_eff, k_n for
-    // contacts of two particles equal to them
-    launch_pack_state(ctx->state[buf], r, static_cast<uint32_t>(n), true, s, &ctx->ctl->r_ref);
+    // contacts of two particles equal to them (kept when radii / masses are kept)
+    launch_pack_state(ctx->state[buf], r, static_cast<uint32_t>(n), true, s,
+                      r.rad && r.mass ? &ctx->ctl->r_ref : nullptr);
     CUDA_TRY(cudaStreamSynchronize(s));
     CUDA_TRY(cudaGetLastError());
     return DEM_OK;
@@ -882,8 +888,7 @@ int dem_get_particles(dem_ctx* ctx, dem_particles* out) {
 
 int dem_set_particles(dem_ctx* ctx, const dem_particles* in) {
     if (!ctx || !in || in->count != ctx->n) return DEM_ERR_ARGUMENT;
-    if (!in->ids || !in->positions || !in->velocities || !in->angular_velocities || !in->radii || !in->masses || !in->material_ids)
-        return DEM_ERR_ARGUMENT;
+    if (!in->positions || !in->velocities || !in->angular_velocities) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
     SETTLE(ctx);
     ctx->replaced_at = ctx->phase_count;  // the binning no longer matches the state (traces)

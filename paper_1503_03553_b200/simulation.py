@@ -206,14 +206,17 @@ class ParticleSet:  # particle_set.hpp:13-37, numpy SoA
 
     def c_struct(self) -> _capi.dem_particles:
         p = _capi.dem_particles()
-        p.count = len(self.ids)
-        p.ids = self.ids.ctypes.data_as(C.POINTER(C.c_uint32))
-        p.positions = self.positions.ctypes.data_as(C.POINTER(C.c_double))
-        p.velocities = self.velocities.ctypes.data_as(C.POINTER(C.c_double))
-        p.angular_velocities = self.angular_velocities.ctypes.data_as(C.POINTER(C.c_double))
-        p.radii = self.radii.ctypes.data_as(C.POINTER(C.c_double))
-        p.masses = self.masses.ctypes.data_as(C.POINTER(C.c_double))
-        p.material_ids = self.material_ids.ctypes.data_as(C.POINTER(C.c_uint32))
+        p.count = len(self.positions)
+
+        def ptr(a, t):  # None -> NULL (dem_get_particles skips it, dem_set_particles keeps it)
+            return None if a is None else a.ctypes.data_as(C.POINTER(t))
+        p.ids = ptr(self.ids, C.c_uint32)
+        p.positions = ptr(self.positions, C.c_double)
+        p.velocities = ptr(self.velocities, C.c_double)
+        p.angular_velocities = ptr(self.angular_velocities, C.c_double)
+        p.radii = ptr(self.radii, C.c_double)
+        p.masses = ptr(self.masses, C.c_double)
+        p.material_ids = ptr(self.material_ids, C.c_uint32)
         return p
 
 
@@ -498,6 +501,19 @@ class Simulation:
     def set_particles(self, s: ParticleSet):
         self._run_pending()
         s = s.contiguous()
+        self._check(self._lib.dem_set_particles(self._ctx, C.byref(s.c_struct())))
+
+    def set_motion(self, positions, velocities, angular_velocities):
+        """Replace only the kinematic state (current slot order, as particles() returns it); ids,
+        radii, masses and materials stay (dem_set_particles with those arrays NULL)."""
+        self._run_pending()
+        s = ParticleSet(0)
+        s.ids = s.radii = s.masses = s.material_ids = None
+        s.positions = np.ascontiguousarray(positions, np.float64).reshape(-1, 3)
+        s.velocities = np.ascontiguousarray(velocities, np.float64).reshape(-1, 3)
+        s.angular_velocities = np.ascontiguousarray(angular_velocities, np.float64).reshape(-1, 3)
+        if len(s.positions) != self.size():
+            raise ValueError("set_motion: arrays must have one row per particle")
         self._check(self._lib.dem_set_particles(self._ctx, C.byref(s.c_struct())))
 
     def forces(self) -> ForceAccumulator:

@@ -82,3 +82,26 @@ def test_async_error_surfaces_at_next_call(cuda):
     assert ea.value.step == eb.value.step
     assert a.step_index() == b.step_index()
     b.particles()  # the context stays usable
+
+
+def test_motion_only_set_and_partial_get(cuda):
+    """dem_set_particles with ids / radii / masses / materials NULL keeps them per slot; the step
+    after it equals the step after a full set, bit for bit. dem_get_particles fills only the
+    arrays it is given."""
+    a, b = _pair(32768, 5)
+    a.steps(2)
+    b.steps(2)
+    full = a.particles()
+    full.positions = full.positions + 1e-7
+    a.set_particles(full)
+    b.set_motion(full.positions, full.velocities, full.angular_velocities)
+    a.step()
+    b.step()
+    _same_state(a, b)
+    part = b.particles()
+    part.radii = part.masses = part.material_ids = None
+    part.positions[:] = 0.0
+    b.particles_into(part)
+    assert bitwise_equal(part.positions, a.particles().positions)
+    with pytest.raises(ValueError):
+        b.set_motion(full.positions[:10], full.velocities[:10], full.angular_velocities[:10])

@@ -68,7 +68,10 @@ def main(tag):
         lines += ["## bench.py (N=1)", "",
                   f"* value **{b['value']:.4g} {b['unit']}**, {b['ms_per_step']:.4f} ms/step, "
                   f"{b['steps']} timed steps, L2 flushed between steps",
-                  f"* e2e (C ABI, host buffers) {b['e2e']['value']:.4g} {b['unit']}",
+                  f"* e2e (C ABI, full state both ways, pinned host buffers, readback overlapping the step) "
+                  f"{b['e2e']['value']:.4g} {b['unit']}"
+                  + (f"; host-coupled motion exchange (72 B up, 76 B down per particle) {b['e2e_motion']['value']:.4g}"
+                     if "e2e_motion" in b else ""),
                   f"* roofline: {b['roofline']['kernel']} {b['roofline']['achieved']:.0f} GB/s = "
                   f"{100 * b['roofline']['frac']:.1f}% of {b['roofline']['peak']} GB/s ({b['roofline']['peak_kind']})",
                   f"* clocks: {b['clocks']}"]

@@ -1,0 +1,130 @@
+"""GPU edge cases of the hot path against the CPU restatement (oracle/): an empty set, a single
+particle, pairs placed ulps around the contact boundary (the exact classification's ambiguous
+band), coincident centres (DegenerateContactError, geometry.cpp:32), a contact row filled to
+exactly K and one past it (CapacityError, contact_table.cpp:15-35), and particle counts that do not
+fill the last 32-slot tile."""
+import numpy as np
+import pytest
+
+from helpers import basic_config, box_for, random_dense_state
+from test_periodic import _compare
+
+import paper_1503_03553_b200 as dem
+
+pytestmark = pytest.mark.gpu
+
+
+def _pair_state(n_pairs, seed):
+    """n_pairs two-particle clusters; in each the centre distance is reach * (1 + k 2^-52),
+    k in -4..4, along a random direction (distance rounding puts some exactly on reach)."""
+    rng = np.random.default_rng(seed)
+    rows = []
+    r = 0.005
+    pid = 0
+    for c in range(n_pairs):
+        k = (c % 9) - 4
+        centre = np.array([0.05 + 0.04 * (c % 10), 0.05 + 0.04 * ((c // 10) % 10), 0.05 + 0.04 * (c // 100)])
+        u = rng.normal(size=3)
+        u /= np.linalg.norm(u)
+        d = 2 * r * (1.0 + k * 2.0 ** -52)
+        a, b = centre - 0.5 * d * u, centre + 0.5 * d * u
+        v = rng.uniform(-0.1, 0.1, 3)
+        rows.append((pid, tuple(a), tuple(v), (0.0, 0.0, 0.0), r, 1e-3, 0))
+        rows.append((pid + 1, tuple(b), tuple(-v), (0.0, 0.0, 0.0), r, 1e-3, 0))
+        pid += 2
+    return dem.ParticleSet.from_lists(rows)
+
+
+def test_empty_set(cuda, orc):
+    from oracle.oracle import OracleSim, OracleError
+    cfg = basic_config(0.1)
+    # no radius to size the cells from (grid.cpp:10-28): a ConfigError in both implementations
+    with pytest.raises(dem.ConfigError):
+        dem.Simulation(dem.ParticleSet(0), cfg)
+    with pytest.raises(OracleError) as eo:
+        OracleSim(orc, dem.ParticleSet(0), cfg)
+    assert eo.value.code == 1
+    cfg.grid_cell_size = 0.01
+    sim = dem.Simulation(dem.ParticleSet(0), cfg)
+    m = sim.step()
+    assert (m.step, m.contacts, m.pp_contact_events) == (1, 0, 0)
+    sim.step_async(2)
+    assert sim.sync().contacts == 0
+    assert sim.step_index() == 3
+    assert len(sim.particles().ids) == 0
+    assert sim.forces().force.shape == (0, 3)
+
+
+@pytest.mark.parametrize("n", [1, 33, 1000])
+def test_ragged_counts_bitwise(cuda, orc, n):
+    """1 particle (free fall), and counts that leave the last tile partly empty."""
+    from oracle.oracle import OracleSim
+    cfg = basic_config(box_for(n))
+    cfg.gravity = (0.0, 0.0, -9.81)
+    ps = random_dense_state(n, 70 + n)
+    sim = dem.Simulation(ps, cfg)
+    osim = OracleSim(orc, ps, cfg)
+    for _ in range(5):
+        m, om = sim.step(), osim.step()
+        assert (m.contacts, m.pp_contact_events) == (om.contacts, om.pp_contact_events)
+    _compare(sim, osim)
+
+
+def test_contact_boundary_ulps(cuda, orc):
+    """Pairs at reach (1 + k 2^-52): contact iff RN(sqrt(d.d)) < reach, decided as the reference
+    does, with forces and histories bitwise."""
+    from oracle.oracle import OracleSim
+    ps = _pair_state(450, 3)
+    cfg = basic_config(0.5)
+    sim = dem.Simulation(ps, cfg)
+    osim = OracleSim(orc, ps, cfg)
+    hits = 0
+    for _ in range(3):
+        m, om = sim.step(), osim.step()
+        assert (m.contacts, m.pp_contact_events) == (om.contacts, om.pp_contact_events)
+        hits += m.pp_contact_events
+    assert 0 < hits < 3 * 450 * 2  # some pairs touch, some do not
+    _compare(sim, osim)
+
+
+def test_coincident_centres_raise_degenerate(cuda, orc):
+    from oracle.oracle import OracleSim, OracleError
+    rows = [(0, (0.05, 0.05, 0.05), (0, 0, 0), (0, 0, 0), 0.005, 1e-3, 0),
+            (1, (0.05, 0.05, 0.05), (0, 0, 0), (0, 0, 0), 0.005, 1e-3, 0),
+            (2, (0.02, 0.02, 0.02), (0, 0, 0), (0, 0, 0), 0.005, 1e-3, 0)]
+    ps = dem.ParticleSet.from_lists(rows)
+    cfg = basic_config(0.1)
+    with pytest.raises(dem.DegenerateContactError) as e:
+        dem.Simulation(ps, cfg)  # the constructor's priming pass detects it
+    assert e.value.kernel == "Collide"
+    with pytest.raises(OracleError) as eo:
+        OracleSim(orc, ps, cfg)
+    assert eo.value.code == 4
+
+
+@pytest.mark.parametrize("k_neighbours,ok", [(4, True), (5, False)])
+def test_capacity_exactly_full_and_one_over(cuda, orc, k_neighbours, ok):
+    """A centre particle touching k neighbours with contact_capacity 4."""
+    from oracle.oracle import OracleSim, OracleError
+    r = 0.005
+    c = np.array([0.05, 0.05, 0.05])
+    dirs = [(1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1)]
+    rows = [(0, tuple(c), (0, 0, 0), (0, 0, 0), r, 1e-3, 0)]
+    for q in range(k_neighbours):
+        rows.append((q + 1, tuple(c + 1.9 * r * np.array(dirs[q], float)), (0, 0, 0), (0, 0, 0), r, 1e-3, 0))
+    ps = dem.ParticleSet.from_lists(rows)
+    cfg = basic_config(0.1)
+    cfg.contact_capacity = 4
+    if ok:
+        sim = dem.Simulation(ps, cfg)
+        osim = OracleSim(orc, ps, cfg)
+        m, om = sim.step(), osim.step()
+        assert m.max_contacts_per_particle == om.max_contacts_per_particle == 4
+        _compare(sim, osim)
+    else:
+        with pytest.raises(dem.CapacityError) as e:
+            dem.Simulation(ps, cfg)
+        assert e.value.kernel == "Collide"
+        with pytest.raises(OracleError) as eo:
+            OracleSim(orc, ps, cfg)
+        assert eo.value.code == 3

@@ -59,6 +59,7 @@ struct dem_ctx {
     double* ft = nullptr;
     uint32_t *key = nullptr, *skey = nullptr, *loc = nullptr, *cnt = nullptr, *cstart = nullptr;
     uint32_t *tmp_src = nullptr, *tmp_id = nullptr, *prev_slot = nullptr;
+    uint2* prev_row = nullptr;
     uint32_t *pair_i = nullptr, *pair_j = nullptr;
     unsigned long long *status_scan = nullptr, *status_det = nullptr;
     uint32_t n_tiles_scan = 0, n_tiles_det = 0;
@@ -314,7 +315,7 @@ PhaseBufs make_bufs(const dem_ctx* c, uint64_t phase) {
     b.cur_h = c->hist[cur];
     b.ft = c->ft;
     b.key = c->key; b.skey = c->skey; b.loc = c->loc; b.cnt = c->cnt; b.cstart = c->cstart;
-    b.tmp_src = c->tmp_src; b.tmp_id = c->tmp_id; b.prev_slot = c->prev_slot;
+    b.tmp_src = c->tmp_src; b.tmp_id = c->tmp_id; b.prev_slot = c->prev_slot; b.prev_row = c->prev_row;
     b.pair_i = c->pair_i; b.pair_j = c->pair_j;
     b.status_scan = c->status_scan; b.status_det = c->status_det;
     b.n_tiles_scan = c->n_tiles_scan; b.n_tiles_det = c->n_tiles_det;
@@ -507,6 +508,7 @@ int allocate(dem_ctx* ctx) {
     CUDA_TRY(dalloc(ctx, &ctx->tmp_src, n));
     CUDA_TRY(dalloc(ctx, &ctx->tmp_id, n));
     CUDA_TRY(dalloc(ctx, &ctx->prev_slot, n));
+    CUDA_TRY(dalloc(ctx, &ctx->prev_row, n));
     CUDA_TRY(dalloc(ctx, &ctx->pair_i, ctx->cap));
     CUDA_TRY(dalloc(ctx, &ctx->pair_j, ctx->cap));
     CUDA_TRY(dalloc(ctx, &ctx->status_scan, ctx->n_tiles_scan + 1));
@@ -761,6 +763,7 @@ int dem_clone(const dem_ctx* src, dem_ctx** out) {
         copy(ctx->skey, src->skey, n * sizeof(uint32_t));
         copy(ctx->cstart, src->cstart, (static_cast<size_t>(src->M) + 1) * sizeof(uint32_t));
         copy(ctx->prev_slot, src->prev_slot, n * sizeof(uint32_t));
+        copy(ctx->prev_row, src->prev_row, n * sizeof(uint2));
         copy(ctx->pair_i, src->pair_i, src->cap * sizeof(uint32_t));
         copy(ctx->pair_j, src->pair_j, src->cap * sizeof(uint32_t));
         copy(ctx->ctl, src->ctl, sizeof(DevCtl));

@@ -109,6 +109,7 @@ struct PhaseBufs {
     uint32_t* tmp_src;       // n
     uint32_t* tmp_id;        // n
     uint32_t* prev_slot;     // n
+    uint2* prev_row;         // n: {pos, cnt} of the slot's previous history row (written by k_reorder)
     uint32_t* pair_i;        // cap
     uint32_t* pair_j;        // cap
     unsigned long long* status_scan;

@@ -230,6 +230,14 @@ int dem_get_order(dem_ctx* ctx, uint32_t* sorted_keys, uint32_t* permutation);
 /* Live contact history after the last force phase (ContactTable touched slots,
  * contact_table.hpp:53-66): owner slot, partner (slot >= 0, or wall id -(w+1)),
  * delta_t (3 per entry), in per-owner accumulation order. Returns the count; fills up to cap. */
+/* Replace the live contact history (the mutable ContactTable the reference's bench restores,
+ * runner.cpp:131-132): `count` entries (owner slot, partner slot >= 0 or wall id -(w+1), delta_t),
+ * in the current slot order; each owner's entries keep their given order. The next force phase
+ * merges tangential history from it exactly as from a history the step produced. Owners with more
+ * than contact_capacity entries, repeated (owner, partner) pairs or out-of-range slots are
+ * DEM_ERR_ARGUMENT. Single-GPU contexts. */
+int dem_set_contacts(dem_ctx* ctx, const uint32_t* owner_slot, const int32_t* partner, const double* delta_t,
+                     int64_t count);
 int64_t dem_get_contacts(dem_ctx* ctx, uint32_t* owner_slot, int32_t* partner, double* delta_t,
                          int64_t cap);
 

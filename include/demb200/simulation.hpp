@@ -474,6 +474,10 @@ class Simulation {
     const ForceAccumulator& forces() const { sync_forces(); return forces_; }
     ForceAccumulator& forces() { sync_forces(); forces_dirty_ = true; return forces_; }
     const ContactTable& contact_table() const { sync_table(); return table_; }
+    /// Mutable, as the reference's bench uses it to restore a saved table (runner.cpp:131-132):
+    /// touched, non-empty slots are uploaded before the next kernel (dem_set_contacts); the
+    /// phase's sweep would delete the untouched ones (contact_table.cpp:37-46).
+    ContactTable& contact_table() { sync_table(); table_dirty_ = true; return table_; }
     const SortedOrder& order() const { sync_order(); return order_; }
     std::int64_t step_index() const { return dem_step_index(ctx_.get()); }
     std::int64_t last_clamp_count() const { run_pending(); return last_.clamps; }
@@ -546,6 +550,21 @@ class Simulation {
         if (forces_dirty_) {
             self->check(dem_set_forces(ctx_.get(), &self->forces_.force[0].x, &self->forces_.torque[0].x));
             self->forces_dirty_ = false;
+        }
+        if (table_dirty_) {
+            std::vector<std::uint32_t> o;
+            std::vector<std::int32_t> pr;
+            std::vector<double> d;
+            for (std::uint32_t i = 0; i < table_.particle_count(); ++i)
+                for (int k = 0; k < table_.capacity(); ++k) {
+                    const ContactSlot& c = table_.row(i)[k];
+                    if (c.empty() || !c.touched) continue;
+                    o.push_back(i);
+                    pr.push_back(c.partner);
+                    d.insert(d.end(), {c.delta_t.x, c.delta_t.y, c.delta_t.z});
+                }
+            self->check(dem_set_contacts(ctx_.get(), o.data(), pr.data(), d.data(), static_cast<std::int64_t>(o.size())));
+            self->table_dirty_ = false;
         }
     }
 
@@ -714,7 +733,7 @@ class Simulation {
     mutable SortedOrder order_;
     mutable bool state_fresh_ = false, forces_fresh_ = false, table_fresh_ = false, traces_fresh_ = false,
                  order_fresh_ = false;
-    mutable bool state_dirty_ = false, forces_dirty_ = false;
+    mutable bool state_dirty_ = false, forces_dirty_ = false, table_dirty_ = false;
     StepMetrics last_;
     bool record_traces_ = true;
 };

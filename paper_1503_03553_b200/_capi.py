@@ -127,6 +127,7 @@ SIGNATURES = [
     ("dem_ipc_handle", C.c_int, [C.c_int, C.c_void_p, C.c_void_p]),
     ("dem_ipc_open", C.c_int, [C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]),
     ("dem_ipc_close", C.c_int, [C.c_int, C.c_void_p]),
+    ("dem_set_contacts", C.c_int, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_int32), C.POINTER(C.c_double), C.c_int64]),
     ("dem_selftest_division", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64)]),
 ]
 

@@ -963,6 +963,50 @@ int dem_get_order(dem_ctx* ctx, uint32_t* sorted_keys, uint32_t* permutation) {
     return DEM_OK;
 }
 
+int dem_set_contacts(dem_ctx* ctx, const uint32_t* owner_slot, const int32_t* partner, const double* delta_t,
+                     int64_t count) {
+    if (!ctx || ctx->slab || count < 0 || (count && (!owner_slot || !partner || !delta_t))) return DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    SETTLE(ctx);
+    const uint64_t n = ctx->n;
+    if (n == 0) return count ? DEM_ERR_ARGUMENT : DEM_OK;
+    const uint32_t K = static_cast<uint32_t>(ctx->K);
+    // stable ids of the current slots: the history keys partners by id (walls by their code)
+    std::vector<uint2> idm(n);
+    CUDA_TRY(cudaMemcpy(idm.data(), ctx->state[state_cur(ctx)].idm, n * sizeof(uint2), cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> cnt(n, 0), pos(n, 0);
+    for (int64_t k = 0; k < count; ++k) {
+        if (owner_slot[k] >= n) return DEM_ERR_ARGUMENT;
+        if (partner[k] >= 0 && static_cast<uint64_t>(partner[k]) >= n) return DEM_ERR_ARGUMENT;
+        if (++cnt[owner_slot[k]] > K) return DEM_ERR_ARGUMENT;
+    }
+    // tile-compacted layout: owner i's row inside tile i/32's region, slot order
+    for (uint64_t t0 = 0; t0 < n; t0 += 32) {
+        uint32_t q = static_cast<uint32_t>(t0 * K);
+        for (uint64_t i = t0; i < std::min<uint64_t>(n, t0 + 32); ++i) { pos[i] = q; q += cnt[i]; }
+    }
+    const size_t cap = ctx->cap;
+    std::vector<uint32_t> key(cap, 0), pj(cap, 0), fill(n, 0);
+    std::vector<double> dt(3 * cap, 0.0);
+    for (int64_t k = 0; k < count; ++k) {
+        const uint32_t i = owner_slot[k];
+        const uint32_t q = pos[i] + fill[i]++;
+        const uint32_t kk = partner[k] >= 0 ? idm[partner[k]].x : static_cast<uint32_t>(partner[k]);
+        for (uint32_t r = pos[i]; r < q; ++r)
+            if (key[r] == kk) return DEM_ERR_ARGUMENT;  // one entry per partner (contact_table.cpp:15-35)
+        key[q] = kk;
+        pj[q] = static_cast<uint32_t>(partner[k]);
+        for (int a = 0; a < 3; ++a) dt[a * cap + q] = delta_t[3 * k + a];
+    }
+    const HistBuf& h = ctx->hist[hist_cur(ctx)];
+    CUDA_TRY(cudaMemcpy(h.pos, pos.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(h.cnt, cnt.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(h.key, key.data(), cap * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(h.dt, dt.data(), 3 * cap * sizeof(double), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(ctx->pair_j, pj.data(), cap * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    return DEM_OK;
+}
+
 int64_t dem_get_contacts(dem_ctx* ctx, uint32_t* owner_slot, int32_t* partner, double* delta_t, int64_t cap) {
     if (!ctx) return -DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);

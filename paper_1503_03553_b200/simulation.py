@@ -555,6 +555,19 @@ class Simulation:
                                             p.ctypes.data_as(C.POINTER(C.c_uint32))))
         return k, p
 
+    def set_contacts(self, owner_slot, partner, delta_t):
+        """Replace the live contact history (current slot order; partners as slots or -(w+1)), as
+        the reference's bench restores its ContactTable (runner.cpp:131-132)."""
+        self._run_pending()
+        o = np.ascontiguousarray(owner_slot, np.uint32)
+        p = np.ascontiguousarray(partner, np.int32)
+        d = np.ascontiguousarray(delta_t, np.float64).reshape(-1, 3)
+        if not (len(o) == len(p) == len(d)):
+            raise ValueError("set_contacts: arrays of different lengths")
+        self._check(self._lib.dem_set_contacts(self._ctx, o.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                               p.ctypes.data_as(C.POINTER(C.c_int32)),
+                                               d.ctypes.data_as(C.POINTER(C.c_double)), len(o)))
+
     def contacts(self):
         """Touched contact-table entries: (owner slot[], partner[] (slot or -(w+1)), delta_t[,3])."""
         cnt = self._lib.dem_get_contacts(self._ctx, None, None, None, 0)

@@ -139,6 +139,24 @@ int main() {
     bsim.step();
     fork.step();
     EXPECT(bsim.particles() == fork.particles());
+    // mutable contact table (runner.cpp:131-132 restores one): a wiped table loses the tangential
+    // history, the saved one restored reproduces the step bit for bit
+    {
+        const b2::ContactTable saved = bsim.contact_table();
+        b2::Simulation wiped = bsim, restored = bsim;
+        bsim.step();
+        wiped.contact_table() = b2::ContactTable(saved.particle_count(), saved.capacity());
+        wiped.step();
+        restored.contact_table() = b2::ContactTable(saved.particle_count(), saved.capacity());
+        restored.contact_table() = saved;
+        restored.step();
+        EXPECT(saved.total_live() > 0);
+        EXPECT(bsim.particles() == restored.particles());
+        bool differs = false;
+        for (std::size_t k = 0; k < n; ++k)
+            differs = differs || std::memcmp(&bsim.forces().force[k], &wiped.forces().force[k], sizeof(b2::Vec3)) != 0;
+        EXPECT(differs);
+    }
     // mutable accessor: a NaN force makes the next Integrate throw KernelError("Integrate")
     bsim.forces().force[3].x = std::nan("");
     bool threw = false;

@@ -204,7 +204,30 @@ class ParticleSet:  # particle_set.hpp:13-37, numpy SoA
         s.material_ids = np.ascontiguousarray(self.material_ids, np.uint32)
         return s
 
+    _FIELDS = (("ids", np.uint32), ("positions", np.float64), ("velocities", np.float64),
+               ("angular_velocities", np.float64), ("radii", np.float64), ("masses", np.float64),
+               ("material_ids", np.uint32))
+
+    def is_contiguous(self) -> bool:
+        """Every present array C-contiguous with the ABI dtype (then c_struct can view it as is)."""
+        for k, dt in self._FIELDS:
+            a = getattr(self, k)
+            if a is not None and (a.dtype != dt or not a.flags.c_contiguous):
+                return False
+        return True
+
     def c_struct(self) -> _capi.dem_particles:
+        # cached per set of array buffers (host-coupled loops pass the same pinned arrays every step)
+        key = tuple(None if getattr(self, k) is None else (getattr(self, k).ctypes.data, getattr(self, k).size)
+                    for k, _ in self._FIELDS)
+        cached = getattr(self, "_c_cache", None)
+        if cached is not None and cached[0] == key:
+            return cached[1]
+        p = self._c_struct_build()
+        self._c_cache = (key, p)
+        return p
+
+    def _c_struct_build(self) -> _capi.dem_particles:
         p = _capi.dem_particles()
         p.count = len(self.positions)
 
@@ -500,15 +523,18 @@ class Simulation:
 
     def set_particles(self, s: ParticleSet):
         self._run_pending()
-        s = s.contiguous()
+        if not s.is_contiguous():
+            s = s.contiguous()
         self._check(self._lib.dem_set_particles(self._ctx, C.byref(s.c_struct())))
 
     def set_motion(self, positions, velocities, angular_velocities):
         """Replace only the kinematic state (current slot order, as particles() returns it); ids,
         radii, masses and materials stay (dem_set_particles with those arrays NULL)."""
         self._run_pending()
-        s = ParticleSet(0)
-        s.ids = s.radii = s.masses = s.material_ids = None
+        s = getattr(self, "_motion", None)
+        if s is None:
+            s = self._motion = ParticleSet(0)
+            s.ids = s.radii = s.masses = s.material_ids = None
         s.positions = np.ascontiguousarray(positions, np.float64).reshape(-1, 3)
         s.velocities = np.ascontiguousarray(velocities, np.float64).reshape(-1, 3)
         s.angular_velocities = np.ascontiguousarray(angular_velocities, np.float64).reshape(-1, 3)

@@ -105,3 +105,24 @@ def test_motion_only_set_and_partial_get(cuda):
     assert bitwise_equal(part.positions, a.particles().positions)
     with pytest.raises(ValueError):
         b.set_motion(full.positions[:10], full.velocities[:10], full.angular_velocities[:10])
+
+
+def test_async_periodic_and_fp32(cuda):
+    """The asynchronous graphs of a periodic Lees-Edwards box and of the fp32 mode."""
+    ps, L = dem.gen_periodic_packing(27000, s=1.8, jit=0.2, seed=8)
+    a, b = dem.Simulation(ps, dem.periodic_config(L, shear_rate=5.0)), dem.Simulation(ps, dem.periodic_config(L, shear_rate=5.0))
+    a.steps(3)
+    b.step_async(3)
+    got = b.particles()
+    assert b.sync().step == a.step_index()
+    want = a.particles()
+    for f in ("positions", "velocities", "angular_velocities"):
+        assert bitwise_equal(getattr(got, f), getattr(want, f)), f
+    assert a.periodic_box() == b.periodic_box()
+    ps2, dmax = dem.gen_packing(27000, s=1.8, jit=0.2, seed=9)
+    cfg = dem.packing_config(dmax)
+    cfg.precision = 1
+    c, d = dem.Simulation(ps2, cfg), dem.Simulation(ps2, cfg)
+    c.steps(2)
+    d.step_async(2)
+    _same_state(c, d)

@@ -336,11 +336,17 @@ class ContactTable {
         for (int s = 0; s < cap_; ++s) k += row(p)[s].empty() ? 0 : 1;
         return k;
     }
+    int max_live_count() const {
+        int m = 0;
+        for (std::uint32_t p = 0; p < n_; ++p) m = std::max(m, live_count(p));
+        return m;
+    }
     std::int64_t total_live() const {
         std::int64_t k = 0;
         for (const auto& s : slots_) k += s.empty() ? 0 : 1;
         return k;
     }
+    bool operator==(const ContactTable&) const = default;
     const ContactSlot* find(std::uint32_t p, std::int32_t partner) const {
         for (int s = 0; s < cap_; ++s)
             if (!row(p)[s].empty() && row(p)[s].partner == partner) return &row(p)[s];
@@ -383,6 +389,39 @@ struct StepMetrics {  // pipeline.hpp:35-48
     std::int64_t capped_contacts = 0;  // new counter: contacts whose friction cap engaged
 };
 
+/// pipeline.hpp:50-53 (pipeline.cpp:31-44): semi-implicit update of a host particle set from
+/// host forces — v += F (dt / m), x += v dt (new v), w += T (dt / I), I = ((0.4 m) r) r; throws
+/// KernelError("Integrate") on a non-finite force or torque, naming the particle. A host utility
+/// like the reference's (the device step integrates inside its own graph); compiled under the
+/// reference's -ffp-contract=off it is bitwise the reference's.
+inline void integrate(ParticleSet& state, const ForceAccumulator& forces, double dt) {
+    const auto finite = [](const Vec3& v) { return std::isfinite(v.x) && std::isfinite(v.y) && std::isfinite(v.z); };
+    for (std::size_t i = 0; i < state.size(); ++i) {
+        const Vec3& f = forces.force[i];
+        const Vec3& t = forces.torque[i];
+        if (!finite(f) || !finite(t))
+            throw KernelError("Integrate", "Integrate: non-finite force on particle " + std::to_string(state.ids[i]));
+        const double s = dt / state.masses[i];
+        Vec3& v = state.velocities[i];
+        v = Vec3{v.x + f.x * s, v.y + f.y * s, v.z + f.z * s};
+        Vec3& x = state.positions[i];
+        x = Vec3{x.x + v.x * dt, x.y + v.y * dt, x.z + v.z * dt};
+        const double inertia = 0.4 * state.masses[i] * state.radii[i] * state.radii[i];
+        const double s2 = dt / inertia;
+        Vec3& w = state.angular_velocities[i];
+        w = Vec3{w.x + t.x * s2, w.y + t.y * s2, w.z + t.z * s2};
+    }
+}
+
+/// pipeline.hpp:55-56 (pipeline.cpp:46-50): F += g m per particle; torques untouched.
+inline void force_gravity(const ParticleSet& state, ForceAccumulator& forces, const Vec3& gravity) {
+    for (std::size_t i = 0; i < state.size(); ++i) {
+        const double m = state.masses[i];
+        Vec3& f = forces.force[i];
+        f = Vec3{f.x + gravity.x * m, f.y + gravity.y * m, f.z + gravity.z * m};
+    }
+}
+
 class Simulation {
   public:
     Simulation(ParticleSet initial, SimConfig config, int device = 0) : cfg_(std::move(config)) {
@@ -392,11 +431,16 @@ class Simulation {
         const int rc = dem_create(&ccfg_, &p, device, &c);
         if (rc != DEM_OK) rethrow(nullptr, rc);
         ctx_.reset(c);
+        double r_max = 0.0;
+        for (double r : initial.radii) r_max = std::max(r_max, r);
+        load_grid(r_max);
         state_ = std::move(initial);
         state_fresh_ = false;
     }
 
     Simulation(const Simulation& o) : cfg_(o.cfg_) {
+        grid_ = o.grid_;
+        neighborhood_sufficient_ = o.neighborhood_sufficient_;
         o.run_pending();
         o.flush();
         build_c_config();
@@ -464,11 +508,10 @@ class Simulation {
     }
 
     const SimConfig& config() const { return cfg_; }
-    UniformGrid grid() const {
-        dem_grid g{};
-        dem_get_grid(ctx_.get(), &g);
-        return UniformGrid{Vec3{g.origin[0], g.origin[1], g.origin[2]}, g.cell_size, g.nx, g.ny, g.nz};
-    }
+    const UniformGrid& grid() const { return grid_; }  // fixed at construction (make_grid, grid.cpp:10-28)
+    /// pipeline.hpp:101-103: the cell size admits the 27-cell neighbourhood guarantee, h >= 2 r_max
+    /// of the initial set (pipeline.cpp:60).
+    bool neighborhood_sufficient() const { return neighborhood_sufficient_; }
     const ParticleSet& particles() const { sync_state(); return state_; }
     ParticleSet& particles() { sync_state(); state_dirty_ = true; return state_; }
     const ForceAccumulator& forces() const { sync_forces(); return forces_; }
@@ -488,6 +531,14 @@ class Simulation {
     }
 
   private:
+    UniformGrid grid_;
+    bool neighborhood_sufficient_ = true;
+    void load_grid(double r_max) {
+        dem_grid g{};
+        check(dem_get_grid(ctx_.get(), &g));
+        grid_ = UniformGrid{Vec3{g.origin[0], g.origin[1], g.origin[2]}, g.cell_size, g.nx, g.ny, g.nz};
+        neighborhood_sufficient_ = grid_.cell_size >= 2.0 * r_max;
+    }
     struct CtxDeleter { void operator()(dem_ctx* c) const { dem_destroy(c); } };
     std::uint32_t pending_ = 0;    // composed per-kernel calls (kernel_integrate ...)
     int pending_last_ = -1;
@@ -587,7 +638,8 @@ class Simulation {
         const auto n = dem_size(ctx_.get());
         self->forces_.force.resize(n);
         self->forces_.torque.resize(n);
-        self->check(dem_get_forces(ctx_.get(), &self->forces_.force[0].x, &self->forces_.torque[0].x));
+        if (n)
+            self->check(dem_get_forces(ctx_.get(), &self->forces_.force.data()->x, &self->forces_.torque.data()->x));
         self->forces_fresh_ = true;
     }
     void sync_table() const {
@@ -596,10 +648,12 @@ class Simulation {
         auto* self = const_cast<Simulation*>(this);
         const auto n = static_cast<std::uint32_t>(dem_size(ctx_.get()));
         const std::int64_t c = dem_get_contacts(ctx_.get(), nullptr, nullptr, nullptr, 0);
+        if (c < 0) self->check(static_cast<int>(c));  // an error code, not a count
         std::vector<std::uint32_t> o(c);
         std::vector<std::int32_t> p(c);
         std::vector<double> d(3 * c);
-        dem_get_contacts(ctx_.get(), o.data(), p.data(), d.data(), c);
+        const std::int64_t c2 = dem_get_contacts(ctx_.get(), o.data(), p.data(), d.data(), c);
+        if (c2 < 0) self->check(static_cast<int>(c2));
         self->table_ = ContactTable(n, cfg_.contact_capacity);
         std::vector<int> fill(n, 0);
         for (std::int64_t k = 0; k < c; ++k) {

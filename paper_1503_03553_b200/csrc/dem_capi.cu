@@ -73,6 +73,8 @@ struct dem_ctx {
     // execution state
     uint64_t phase_count = 0;  // force phases executed (parity selects buffers)
     uint64_t replaced_at = ~0ull;  // phase_count when dem_set_particles last replaced the state
+    bool state_invalid = false;     // the last upload was rejected (REQUIRE_STATE)
+    std::vector<uint32_t> checked_ids;  // the ids last checked unique (check_unique_ids)
     int64_t step_index = 0;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     cudaGraphExec_t graph_async[2] = {nullptr, nullptr};  // + the state-ready event node (dem_step_async)
@@ -186,7 +188,10 @@ int validate(const dem_config* cfg, const dem_particles* p, std::string* why) {
     if (cfg->precision == 1 && cfg->collide_variant == 0)
         return fail("the fp32 throughput mode runs the two_phase collide variant");
     if (cfg->contact_capacity < 1) return fail("contacts.capacity: must be >= 1");
-    if (cfg->contact_capacity > 384) return fail("contacts.capacity: B200 build supports at most 384");
+    // k_detect stages 2K + 1 partner words + up to 38 row bounds per thread (256 threads) in its
+    // 200 KB of shared memory: K <= 80 holds in periodic and walled boxes
+    if (cfg->contact_capacity > kMaxContactCapacity)
+        return fail("contacts.capacity: the B200 build supports at most " + std::to_string(kMaxContactCapacity));
     if (cfg->rect_wall_count + cfg->line_wall_count > static_cast<uint32_t>(kMaxWalls)) return fail("too many walls (max 64)");
     for (uint32_t k = 0; k < cfg->rect_wall_count; ++k) {
         const dem_rect_wall& w = cfg->rect_walls[k];
@@ -456,6 +461,13 @@ int settle(dem_ctx* ctx) {
         const int settle_rc_ = settle(ctx);          \
         if (settle_rc_ != DEM_OK) return settle_rc_; \
     } while (0)
+// entry points that run phases on the state: refused after a rejected dem_set_particles
+#define REQUIRE_STATE(ctx)                                                                          \
+    do {                                                                                            \
+        if ((ctx)->state_invalid)                                                                   \
+            return set_error(ctx, DEM_ERR_CONFIG, -1, 0, 0, (ctx)->step_index,                      \
+                             "particle state was rejected by dem_set_particles; upload a valid one"); \
+    } while (0)
 
 void free_ctx(dem_ctx* c) {
     if (!c) return;
@@ -610,10 +622,50 @@ int upload_state(dem_ctx* ctx, const dem_particles* p, int buf) {
     // + r_ref, m_ref = particle 0's radius and mass: the monodisperse detection shortcut compares
     // every radius with r_ref (k_integrate_hash); k_force_reduce memoises r_eff, m_eff, k_n for
     // contacts of two particles equal to them (kept when radii / masses are kept)
-    launch_pack_state(ctx->state[buf], r, static_cast<uint32_t>(n), true, s,
-                      r.rad && r.mass ? &ctx->ctl->r_ref : nullptr);
+    // every packed particle is validated on the device as it is packed (ParticleSet::validate,
+    // particle_set.cpp:40-58; material ids < count, since they index the force kernel's shared
+    // material table; stable ids below the wall keys): free for the host-coupled stepping loop
+    CUDA_TRY(cudaMemsetAsync(&ctx->ctl->bad_upload, 0xff, sizeof(unsigned long long), s));
+    launch_pack_state(ctx->state[buf], r, static_cast<uint32_t>(n), true, s, ctx->ctl,
+                      static_cast<uint32_t>(ctx->materials.size()), r.rad && r.mass ? &ctx->ctl->r_ref : nullptr);
+    unsigned long long bad = ~0ull;
+    CUDA_TRY(cudaMemcpyAsync(&bad, &ctx->ctl->bad_upload, sizeof(bad), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     CUDA_TRY(cudaGetLastError());
+    if (bad != ~0ull) {
+        // the buffer now holds the rejected particles: no phase may run on it until a valid upload
+        ctx->state_invalid = true;
+        const uint64_t slot = bad >> 8;
+        static const char* const why[] = {"?", "radius must be > 0", "mass must be > 0", "non-finite state",
+                                          "bad material", "stable id in the reserved wall-key range (>= 0xFFFFFFC0)"};
+        const uint32_t code = static_cast<uint32_t>(bad & 0xff);
+        const uint32_t id = p->ids ? p->ids[slot] : 0u;
+        return set_error(ctx, DEM_ERR_CONFIG, -1, static_cast<uint32_t>(slot), id, ctx->step_index,
+                         "particle " + std::to_string(id) + ": " + why[code < 6 ? code : 0]);
+    }
+    ctx->state_invalid = false;
+    return DEM_OK;
+}
+
+// ParticleSet ids must be unique for the B200 path: its contact history is keyed by the partner's
+// stable id (the reference keys it by slot, contact_table.hpp:16-24). O(n log n) on a copy; a
+// re-upload of the ids last checked skips the sort (one memcmp).
+int check_unique_ids(const uint32_t* ids, uint64_t n, std::vector<uint32_t>* cache, std::string* why) {
+    if (!ids) return DEM_OK;
+    if (cache && cache->size() == n && (n == 0 || std::memcmp(cache->data(), ids, n * sizeof(uint32_t)) == 0))
+        return DEM_OK;
+    std::vector<uint32_t> v(ids, ids + n);
+    std::sort(v.begin(), v.end());
+    const auto d = std::adjacent_find(v.begin(), v.end());
+    if (d != v.end()) {
+        *why = "particle " + std::to_string(*d) + ": duplicate stable id (the B200 contact history is keyed by id)";
+        return DEM_ERR_CONFIG;
+    }
+    if (n && v.back() > 0xFFFFFFBFu) {
+        *why = "particle " + std::to_string(v.back()) + ": stable id in the reserved wall-key range (>= 0xFFFFFFC0)";
+        return DEM_ERR_CONFIG;
+    }
+    if (cache) cache->assign(ids, ids + n);
     return DEM_OK;
 }
 
@@ -651,6 +703,7 @@ int dem_create(const dem_config* cfg, const dem_particles* particles, int device
     *out = nullptr;
     std::string why;
     int rc = validate(cfg, particles, &why);
+    if (rc == DEM_OK) rc = check_unique_ids(particles->ids, particles->count, nullptr, &why);
     if (rc != DEM_OK) {
         std::snprintf(g_create_error.message, sizeof(g_create_error.message), "%s", why.c_str());
         g_create_error.code = rc;
@@ -775,6 +828,8 @@ int dem_clone(const dem_ctx* src, dem_ctx** out) {
     }
     ctx->phase_count = src->phase_count;
     ctx->replaced_at = src->replaced_at;
+    ctx->state_invalid = src->state_invalid;
+    ctx->checked_ids = src->checked_ids;
     ctx->step_index = src->step_index;
     ctx->last_error = src->last_error;
     if (rc == DEM_OK) rc = build_graphs(ctx);
@@ -789,6 +844,7 @@ int dem_step(dem_ctx* ctx, int nsteps, dem_step_metrics* last) {
     if (!ctx || nsteps < 0) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
     SETTLE(ctx);
+    REQUIRE_STATE(ctx);
     if (ctx->n == 0) {
         ctx->step_index += nsteps;
         if (last) { std::memset(last, 0, sizeof(*last)); last->step = ctx->step_index; }
@@ -807,6 +863,7 @@ int dem_step(dem_ctx* ctx, int nsteps, dem_step_metrics* last) {
 int dem_step_async(dem_ctx* ctx, int nsteps) {
     if (!ctx || nsteps < 0 || ctx->slab) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
+    REQUIRE_STATE(ctx);
     if (ctx->n == 0) {
         ctx->step_index += nsteps;
         return DEM_OK;
@@ -836,6 +893,8 @@ int dem_force_phase(dem_ctx* ctx, uint32_t flags, dem_step_metrics* m) {
     if (!ctx || (flags & ~static_cast<uint32_t>(DEM_PHASE_STEP))) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
     SETTLE(ctx);
+    REQUIRE_STATE(ctx);
+    REQUIRE_STATE(ctx);
     return run_phase(ctx, flags, m, flags == DEM_PHASE_STEP);
 }
 
@@ -894,6 +953,9 @@ int dem_set_particles(dem_ctx* ctx, const dem_particles* in) {
     if (!in->positions || !in->velocities || !in->angular_velocities) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
     SETTLE(ctx);
+    std::string why;
+    if (check_unique_ids(in->ids, in->count, &ctx->checked_ids, &why) != DEM_OK)
+        return set_error(ctx, DEM_ERR_CONFIG, -1, 0, 0, ctx->step_index, why);
     ctx->replaced_at = ctx->phase_count;  // the binning no longer matches the state (traces)
     return upload_state(ctx, in, state_cur(ctx));
 }
@@ -1092,6 +1154,7 @@ int dem_time_steps(dem_ctx* ctx, int nsteps, size_t flush_bytes, float* step_ms,
     if (!ctx || nsteps < 0 || (nsteps && !step_ms)) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
     SETTLE(ctx);
+    REQUIRE_STATE(ctx);
     if (flush_bytes && flush_bytes != ctx->flush_bytes) {
         if (ctx->flush_buf) cudaFree(ctx->flush_buf);
         ctx->flush_buf = nullptr;
@@ -1120,6 +1183,7 @@ int dem_profile_step(dem_ctx* ctx, size_t flush_bytes, dem_step_metrics* m) {
     if (!ctx || !m) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
     SETTLE(ctx);
+    REQUIRE_STATE(ctx);
     if (flush_bytes && flush_bytes != ctx->flush_bytes) {
         if (ctx->flush_buf) cudaFree(ctx->flush_buf);
         ctx->flush_buf = nullptr;

@@ -11,6 +11,7 @@ namespace demb200 {
 
 constexpr int kMaxMaterials = 16;
 constexpr int kMaxWalls = 64;
+constexpr int kMaxContactCapacity = 80;  // k_detect's shared-memory rows (dem_kernels.cu launch_detect)
 constexpr uint32_t kWallBit = 0x80000000u;  // partner codes >= this are walls: ~code = wall index
 constexpr unsigned long long kNoError = ~0ull;
 constexpr uint32_t kPhaseSlab = 64u;  // internal phase flag: slab context (ghost-aware kernels)
@@ -76,6 +77,7 @@ struct DevCtl {
     double m_ref;                               // its mass (force memo); must follow r_ref
     long long le_steps;                         // integrating phases so far (Lees-Edwards clock)
     double le_delta;                            // Lees-Edwards image offset of the upper box
+    unsigned long long bad_upload;              // (slot<<8)|reason of the first invalid uploaded particle, atomicMin
 };
 
 // Structure-of-arrays particle state for one buffer (sorted slot order).
@@ -175,9 +177,11 @@ struct RawState {
     double *pos, *vel, *omg, *rad, *mass;
     uint32_t *ids, *mat;
 };
-// pack: host layout -> SoA, and (ref non-null) ref[0], ref[1] = particle 0's radius and mass
+// pack: host layout -> SoA, and (ref non-null) ref[0], ref[1] = particle 0's radius and mass; with
+// `check`, every packed particle is validated (ParticleSet::validate, particle_set.cpp:40-58, plus
+// the B200 id range) and the first invalid slot lands in check->bad_upload
 void launch_pack_state(const StateBuf& s, const RawState& r, uint32_t n, bool pack, cudaStream_t st,
-                       double* ref = nullptr);
+                       DevCtl* check = nullptr, uint32_t nmat = 0, double* ref = nullptr);
 void launch_ft_layout(double* ft, uint32_t stride, double* f, double* t, uint32_t n, bool to_interleaved, cudaStream_t st);
 cudaError_t init_device_attributes();
 

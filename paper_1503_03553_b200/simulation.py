@@ -517,7 +517,20 @@ class Simulation:
         return s
 
     def particles_into(self, s: ParticleSet) -> ParticleSet:
-        """particles() into caller-owned (e.g. pinned) contiguous arrays of the right size."""
+        """particles() into caller-owned (e.g. pinned) contiguous arrays of the right size.
+        The arrays are written through raw pointers, so their dtype, contiguity and size are
+        checked first (ValueError), never trusted."""
+        self._run_pending()
+        n = self.size()
+        if not s.is_contiguous():
+            raise ValueError("particles_into: every array must be C-contiguous with the ABI dtype")
+        for k, _ in ParticleSet._FIELDS:
+            a = getattr(s, k)
+            if a is None:
+                continue
+            per = 3 if k in ("positions", "velocities", "angular_velocities") else 1
+            if a.size != per * n:
+                raise ValueError(f"particles_into: {k} has {a.size} elements, expected {per * n}")
         self._check(self._lib.dem_get_particles(self._ctx, C.byref(s.c_struct())))
         return s
 

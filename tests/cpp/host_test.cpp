@@ -10,7 +10,9 @@
 #include <sstream>
 
 #include "demb200/host.hpp"
+#include "demb200/simulation.hpp"
 #include "demforge/config_io.hpp"
+#include "demforge/pipeline.hpp"
 #include "demforge/error.hpp"
 #include "demforge/lattice.hpp"
 #include "demforge/snapshot_io.hpp"
@@ -159,6 +161,43 @@ int main(int argc, char** argv) {
         bool threw = false;
         try { bad.validate(); } catch (const demb200::ConfigError& e) { threw = std::string(e.what()) == "simt.c_force must exceed simt.c_check"; }
         EXPECT(threw);
+    }
+    {
+        // the free functions of pipeline.hpp:50-56 (host utilities in both): bitwise equal, and the
+        // same KernelError on a non-finite force
+        std::mt19937_64 rng(11);
+        std::uniform_real_distribution<double> u(-1.0, 1.0);
+        demforge::ParticleSet rs;
+        demb200::ParticleSet bs;
+        demforge::ForceAccumulator rf;
+        demb200::ForceAccumulator bf;
+        for (std::uint32_t i = 0; i < 257; ++i) {
+            const double p[3] = {u(rng), u(rng), u(rng)}, v[3] = {u(rng), u(rng), u(rng)}, w[3] = {u(rng), u(rng), u(rng)};
+            const double r = 0.004 + 0.001 * std::abs(u(rng)), m = 1e-3 * (1.5 + u(rng));
+            rs.push_back(i, {p[0], p[1], p[2]}, {v[0], v[1], v[2]}, {w[0], w[1], w[2]}, r, m, 0);
+            bs.push_back(i, {p[0], p[1], p[2]}, {v[0], v[1], v[2]}, {w[0], w[1], w[2]}, r, m, 0);
+            const double f[3] = {u(rng), u(rng), u(rng)}, t[3] = {1e-3 * u(rng), 1e-3 * u(rng), 1e-3 * u(rng)};
+            rf.force.push_back({f[0], f[1], f[2]}); rf.torque.push_back({t[0], t[1], t[2]});
+            bf.force.push_back({f[0], f[1], f[2]}); bf.torque.push_back({t[0], t[1], t[2]});
+        }
+        demforge::force_gravity(rs, rf, {0.1, -0.2, -9.81});
+        demb200::force_gravity(bs, bf, {0.1, -0.2, -9.81});
+        for (int k = 0; k < 3; ++k) {
+            demforge::integrate(rs, rf, 1e-4);
+            demb200::integrate(bs, bf, 1e-4);
+        }
+        bool eq = true;
+        for (std::size_t i = 0; i < rs.size(); ++i)
+            eq = eq && same3(rf.force[i], bf.force[i]) && same3(rs.positions[i], bs.positions[i]) &&
+                 same3(rs.velocities[i], bs.velocities[i]) && same3(rs.angular_velocities[i], bs.angular_velocities[i]);
+        EXPECT(eq);
+        rf.torque[9].y = NAN;
+        bf.torque[9].y = NAN;
+        std::string rw, bw;
+        try { demforge::integrate(rs, rf, 1e-4); } catch (const demforge::KernelError& e) { rw = std::string(e.kernel()) + ":" + e.what(); }
+        try { demb200::integrate(bs, bf, 1e-4); } catch (const demb200::KernelError& e) { bw = e.kernel() + ":" + e.what(); }
+        if (rw != bw) std::printf("reference: %s\nb200:      %s\n", rw.c_str(), bw.c_str());
+        EXPECT(!rw.empty() && rw == bw);
     }
     std::printf("%s\n", failures ? "FAILED" : "PASSED");
     return failures ? 1 : 0;

@@ -107,6 +107,25 @@ def test_config_validation_before_device():
     assert "non-finite" in _expect_config_error(basic_config(1.0), bad)
 
 
+def test_id_and_capacity_validation_before_device():
+    """The B200 history is keyed by stable id: duplicate ids and ids in the wall-key
+    range are rejected (the reference keys its table by slot and accepts them); contact capacity is
+    bounded by k_detect's shared-memory rows (K <= 80)."""
+    from helpers import basic_config, random_dense_state
+    ps = random_dense_state(8, 1)
+    ps.ids[5] = ps.ids[2]
+    assert "duplicate stable id" in _expect_config_error(basic_config(1.0), ps)
+    ps = random_dense_state(8, 1)
+    ps.ids[7] = 0xFFFFFFC0
+    assert "wall-key range" in _expect_config_error(basic_config(1.0), ps)
+    ps = random_dense_state(8, 1)
+    ps.material_ids[1] = 3
+    assert "bad material" in _expect_config_error(basic_config(1.0), ps)
+    cfg = basic_config(1.0)
+    cfg.contact_capacity = 81
+    assert "at most 80" in _expect_config_error(cfg, random_dense_state(8, 1))
+
+
 def test_material_table_rules():
     """materials.cpp:58-68: pair restitution default sqrt(ea eb), overrides symmetric; mu."""
     import paper_1503_03553_b200 as dem

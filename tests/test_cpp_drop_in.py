@@ -17,3 +17,15 @@ def test_cpp_drop_in_side_by_side(cuda):
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "PASSED" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_namespace_alias_switch(cuda):
+    """tests/cpp/alias_test.cpp: a reference-API program compiled with `namespace demforge =
+    demb200;` — every member and free function of pipeline.hpp:50-107 with the reference's types."""
+    binp = os.path.join(HERE, "cpp", "alias_test")
+    if not os.path.exists(binp):
+        pytest.skip("tests/cpp/alias_test not built")
+    r = subprocess.run([binp], capture_output=True, text=True, timeout=300)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0 and "PASSED" in r.stdout, r.stdout + r.stderr

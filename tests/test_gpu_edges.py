@@ -128,3 +128,54 @@ def test_capacity_exactly_full_and_one_over(cuda, orc, k_neighbours, ok):
         with pytest.raises(OracleError) as eo:
             OracleSim(orc, ps, cfg)
         assert eo.value.code == 3
+
+
+def test_set_particles_validates_on_device(cuda):
+    """dem_set_particles validates every uploaded particle (ParticleSet::validate,
+    particle_set.cpp:40-58, plus unique ids below the wall keys): a rejected upload raises
+    ConfigError and the context refuses to step until a valid state is uploaded."""
+    cfg = basic_config(box_for(64))
+    ps = random_dense_state(64, 5)
+    sim = dem.Simulation(ps, cfg)
+    sim.step()
+    good = sim.particles()
+    for field, value, msg in (("material_ids", 7, "bad material"), ("radii", -1.0, "radius"),
+                              ("masses", 0.0, "mass"), ("velocities", np.inf, "non-finite"),
+                              ("ids", 0xFFFFFFF0, "wall-key")):
+        bad = good.copy()
+        getattr(bad, field)[11] = value
+        with pytest.raises(dem.ConfigError, match=msg):
+            sim.set_particles(bad)
+        with pytest.raises(dem.ConfigError):
+            sim.step()
+        sim.set_particles(good)
+        sim.step()
+    dup = good.copy()
+    dup.ids[3] = dup.ids[4]
+    with pytest.raises(dem.ConfigError, match="duplicate"):
+        sim.set_particles(dup)
+    sim.step()  # rejected on the host before any upload: the state is untouched
+    # particles_into checks the caller's arrays before writing through their pointers
+    out = dem.ParticleSet(64)
+    out.positions = np.zeros((64, 3), np.float32)
+    with pytest.raises(ValueError):
+        sim.particles_into(out)
+    out = dem.ParticleSet(63)
+    with pytest.raises(ValueError):
+        sim.particles_into(out)
+    assert sim.particles_into(dem.ParticleSet(64)).size() == 64
+
+
+@pytest.mark.parametrize("periodic", [0, 7])
+def test_largest_contact_capacity(cuda, orc, periodic):
+    """The largest accepted row capacity (K = 80, k_detect's shared-memory bound) runs."""
+    n = 512
+    cfg = basic_config(box_for(n))
+    cfg.contact_capacity = 80
+    cfg.periodic = periodic
+    if periodic:
+        cfg.gravity = (0.0, 0.0, 0.0)
+    ps = random_dense_state(n, 9)
+    sim = dem.Simulation(ps, cfg)
+    m = sim.step()
+    assert m.contacts > 0

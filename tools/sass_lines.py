@@ -53,7 +53,8 @@ def main():
         per_line[loc][0] += e
         per_line[loc][1] += s
         per_line[loc][2] += t
-        per_op[r[1].split()[0].lstrip("@!P0123456789T ").split(".")[0] if r[1].split() else "?"] += e
+        toks = [t for t in r[1].split() if not t.startswith("@")]
+        per_op[toks[0].split(".")[0] if toks else "?"] += e
         tot[0] += e; tot[1] += s; tot[2] += t
     print(f"total warp insts {tot[0]:.4g}  samples {tot[1]}  thread insts/warp inst {tot[2]/max(tot[0],1):.1f}")
     print("-- by executed warp instructions --")

@@ -158,6 +158,13 @@ def pinned_particles(n):
     return ps
 
 
+# The N=1 workload, identical in both arms (the driver compares the two `config` dicts).
+CONFIG_N1 = {"workload": "262,144 monodisperse spheres, dense random packing (configs[1])",
+             "generator": "G(262144, s=1.8, jit=0.2, mono, seed=1)", "dt": 1e-5,
+             "contact_capacity": 16, "parallelism": "single-gpu",
+             "l2": "flushed before every timed step (512 MiB write), outside the events"}
+
+
 def workload(seed=1):
     import paper_1503_03553_b200 as dem
     ps, dmax = dem.gen_packing(N_PARTICLES, s=1.8, jit=0.2, poly=False, seed=seed)
@@ -165,12 +172,36 @@ def workload(seed=1):
     return ps, cfg
 
 
+def reference_workload(seed=1):
+    """The same arrays built by the oracle's copy of the generator: the reference legs never load
+    the product library (oracle/workload.py; bitwise equal, tests/test_oracle_golden.py)."""
+    from oracle.workload import gen_packing, packing_config
+    ps, dmax = gen_packing(N_PARTICLES, s=1.8, jit=0.2, poly=False, seed=seed)
+    return ps, packing_config(dmax)
+
+
+def host_info():
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count()
+    return {"cpu_model": model, "nproc": usable, "logical_cpus": os.cpu_count()}
+
+
 def cpu_reference_run(ps, cfg, steps, warmup, budget_s, threads=None):
-    """Reference Simulation::step() on host cores (oracle/_ref). Returns dict."""
+    """Reference Simulation::step() on host cores (oracle/_ref). Returns dict. `threads` sets the
+    reference's pool size (DEMFORGE_THREADS semantics, parallel.cpp:14-33); None = all cores."""
     from oracle.oracle import RefLib, RefSim
     ref = RefLib()
-    if threads:
-        ref.set_threads(threads)
+    ref.set_threads(threads if threads else host_info()["nproc"])
     cores = ref.thread_count()
     t0 = time.perf_counter()
     sim = RefSim(ref, ps, cfg)  # priming pass untimed, pipeline.cpp:83
@@ -189,28 +220,51 @@ def cpu_reference_run(ps, cfg, steps, warmup, budget_s, threads=None):
     return {"value": value, "steps": done, "seconds": t_total, "cores": cores, "ctor_s": t_ctor}
 
 
+def cpu_baseline_block(ps, cfg, steps, warmup, budget_s):
+    """All host threads, then one thread (both, with the CPU model and core count)."""
+    info = host_info()
+    r = cpu_reference_run(ps, cfg, steps, warmup, budget_s)
+    r1 = cpu_reference_run(ps, cfg, 3, 0, float(os.environ.get("DEM_CPU1_BUDGET_S", "10")), threads=1)
+    block = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "reference",
+             "sample": f"{r['steps']} full steps of the same 262,144-particle workload "
+                       f"({r['seconds']:.1f} s) through the reference Simulation::step() compiled from "
+                       f"its sources (oracle/_ref), DEMFORGE threads={r['cores']}",
+             "threads1": {"value": r1["value"], "unit": UNIT, "cores": 1,
+                          "sample": f"{r1['steps']} steps ({r1['seconds']:.1f} s), DEMFORGE threads=1"},
+             **info}
+    return r, block
+
+
 def run_reference(args):
+    """--impl reference: the reference's own CPU Simulation::step() on this host's cores, on the
+    b200 arm's workload/config/metric, exactly --steps timed after --warmup untimed steps. Inputs
+    come from the oracle's generator copy; nothing from paper_1503_03553_b200 is loaded."""
     world, rank, local = dist_env()
     if rank != 0:
         return 0
-    ps, cfg = workload()
-    budget = float(os.environ.get("DEM_REF_BUDGET_S", "120"))
-    r = cpu_reference_run(ps, cfg, args.steps, min(args.warmup, 1), budget)
+    ps, cfg = reference_workload()
+    r, block = cpu_baseline_block(ps, cfg, args.steps, args.warmup, float("inf"))
     line = {
         "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
-        "n_gpus": args.gpus, "steps": r["steps"], "warmup": min(args.warmup, 1),
+        "n_gpus": args.gpus, "steps": r["steps"], "warmup": args.warmup,
         "ms_per_step": 1e3 * r["seconds"] / r["steps"], "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "262,144 monodisperse spheres, dense random packing (configs[1])",
-                   "generator": "G(262144, s=1.8, jit=0.2, mono, seed=1)", "dt": 1e-5,
-                   "contact_capacity": 16, "parallelism": "cpu-threads"},
-        "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "reference",
-                         "sample": f"{r['steps']} full steps of the 262,144-particle workload "
-                                   f"({r['seconds']:.1f} s), DEMFORGE threads={r['cores']}"},
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY §8d generator, xorshift64*)",
+        "config": dict(CONFIG_N1) if world == 1 else slab_config(world),
+        "cpu_baseline": block,
         "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def slab_config(world):
+    """The N > 1 workload (identical in both arms)."""
+    n_total = N_PARTICLES * world
+    return {"workload": f"{n_total:,} monodisperse spheres, dense packing = configs[1] per GPU",
+            "generator": f"G({n_total}, s=1.8, jit=0.2, mono, seed=1)", "dt": 1e-5,
+            "contact_capacity": 16, "parallelism": f"z-slabs x{world}",
+            "l2": "flushed before every timed step, outside the events"}
 
 
 def run_slab(args, world, rank, local):
@@ -284,12 +338,9 @@ def run_slab(args, world, rank, local):
         "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (SURVEY §8d generator, xorshift64*)",
-        "config": {"workload": f"{n_total:,} monodisperse spheres, dense packing = configs[1] per GPU",
-                   "generator": f"G({n_total}, s=1.8, jit=0.2, mono, seed=1)", "dt": 1e-5,
-                   "contact_capacity": 16, "contacts_per_step": int(c_all.item()),
-                   "parallelism": f"z-slabs x{world}, halo + migration via "
-                                  + ("NVLink peer-memory stores (CUDA IPC)" if transport == "peer" else "NCCL P2P"),
-                   "slabs": bounds, "l2": "flushed before every timed step, outside the events"},
+        "config": slab_config(world),
+        "workload_stats": {"contacts_per_step": int(c_all.item()), "slabs": bounds,
+                           "transport": "NVLink peer-memory stores (CUDA IPC)" if transport == "peer" else "NCCL P2P"},
         "gpu_launches": 11 * args.steps,
         "e2e": {"value": n_total * len(t_e2e) / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": int(d2h / len(t_e2e)),
@@ -300,6 +351,42 @@ def run_slab(args, world, rank, local):
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
     return 0
+
+
+def north_star_block(args):
+    """north_star's target workload on this one GPU: 32M dense frictional spheres (G(33554432,
+    s=1.8, jit=0.2, mono, seed=5), mu = 0.3, K = 16), fp64, its own warm-up / timed steps (CUDA
+    events, L2 flushed), clocks and force-kernel roofline. A second measured block; the headline
+    `value` stays configs[1]."""
+    import paper_1503_03553_b200 as dem
+    n = 1 << 25
+    ps, dmax = dem.gen_packing(n, s=1.8, jit=0.2, poly=False, seed=5)
+    sim = dem.Simulation(ps, dem.packing_config(dmax), device=0)
+    del ps
+    steps = max(3, min(args.steps, 10))
+    for _ in range(3):
+        sim.step()
+    with ClockSampler(0) as clk:
+        step_ms, m = sim.time_steps(steps, FLUSH_BYTES)
+    prof = [sim.profile_step(FLUSH_BYTES) for _ in range(2)]
+    names = dem.device_kernel_names()
+    kms = {nm: statistics.median(p.device_kernel_ms[k] for p in prof) for k, nm in enumerate(names)}
+    c = prof[-1].contacts
+    nbytes = algorithmic_bytes(n, c, prof[-1].cells)
+    peak, peak_kind = peaks()
+    fa = nbytes["k_force_reduce"] / (kms["k_force_reduce"] * 1e-3) / 1e9
+    total_s = sum(step_ms) / 1e3
+    del sim
+    return {"workload": "33,554,432 monodisperse spheres, dense frictional packing (north_star target, configs[4] s=1.8)",
+            "generator": "G(33554432, s=1.8, jit=0.2, mono, seed=5)", "dtype": "f64", "contact_capacity": 16,
+            "value": n * steps / total_s, "unit": UNIT, "steps": steps, "warmup": 3,
+            "ms_per_step": 1e3 * total_s / steps, "contacts_per_step": c, "cells": prof[-1].cells,
+            "capped_contacts": int(prof[-1].capped_contacts), "friction_max_ratio": prof[-1].friction_max_ratio,
+            "roofline": {"bound": "hbm", "kernel": "k_force_reduce", "achieved": fa, "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": fa / peak,
+                         "algorithmic_bytes": nbytes["k_force_reduce"], "ms": kms["k_force_reduce"]},
+            "kernel_ms": kms, "clocks": clk.summary(),
+            "l2": "flushed before every timed step (512 MiB write), outside the events"}
 
 
 def run_b200(args):
@@ -412,11 +499,8 @@ def run_b200(args):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (SURVEY §8d generator, xorshift64*)",
-        "config": {"workload": "262,144 monodisperse spheres, dense random packing (configs[1])",
-                   "generator": "G(262144, s=1.8, jit=0.2, mono, seed=1+rank)", "dt": 1e-5,
-                   "contact_capacity": 16, "contacts_per_step": c, "cells": prof[-1].cells,
-                   "parallelism": "single-gpu",
-                   "l2": "flushed before every timed step (512 MiB write), outside the events"},
+        "config": dict(CONFIG_N1),
+        "workload_stats": {"particles": n, "contacts_per_step": c, "cells": prof[-1].cells, "radix_passes": 1},
         "gpu_launches": sim.kernels_per_step() * args.steps,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": state_bytes,
                 "d2h_bytes_per_step": state_bytes,
@@ -431,15 +515,14 @@ def run_b200(args):
         "kernel_ms": kms,
         "clocks": clk.summary(),
     }
+    del sim
+    if world == 1 and not args.no_north_star:
+        line["north_star_32m"] = north_star_block(args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            budget = float(os.environ.get("DEM_CPU_BUDGET_S", "20"))
-            r = cpu_reference_run(ps, cfg, 1000, 0, budget)
-            line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": r["cores"],
-                                    "kind": "reference",
-                                    "sample": f"{r['steps']} full steps of the same 262,144-particle "
-                                              f"workload ({r['seconds']:.1f} s) through the reference "
-                                              f"Simulation::step() compiled from its sources"}
+            rps, rcfg = reference_workload()
+            _, line["cpu_baseline"] = cpu_baseline_block(rps, rcfg, 1000, 0,
+                                                         float(os.environ.get("DEM_CPU_BUDGET_S", "20")))
         except Exception as e:  # noqa: BLE001
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(),
                                     "kind": "reference", "sample": f"unavailable: {e}"}
@@ -455,9 +538,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-north-star", action="store_true", help="skip the 32M north-star block (N=1)")
     args = ap.parse_args()
-    if args.warmup < 3 and args.impl == "b200":
-        args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
     return run_b200(args)

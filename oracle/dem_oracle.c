@@ -1003,3 +1003,54 @@ void orc_sim_get_pbox(const orc_sim* s, double ext[3], double* off, int64_t* ste
     if (off) *off = s->pb.delta;
     if (steps) *steps = s->pb.le_steps;
 }
+
+/* ---- bench input generator (TEST INFRASTRUCTURE: the reference arm builds its inputs here so it
+ * never loads the product library) ---------------------------------------------------------------
+ * SURVEY.md §8d's G(N, s, jit, poly, seed): the reference benchmark packing shape
+ * (benchmarks/bench_support.hpp:10-44) drawn with the reference's xorshift64* (rng.hpp:11-33).
+ * Draw order per particle: jx, jy, jz, [r], vx, vy, vz, wx, wy, wz. Bitwise the same arrays as the
+ * product's dem_gen_packing (tests/test_oracle_golden.py checks it). */
+static uint64_t orc_xs_next(uint64_t* st) {                              /* rng.hpp:19-26 */
+    uint64_t x = *st;
+    x ^= x >> 12;
+    x ^= x << 25;
+    x ^= x >> 27;
+    *st = x;
+    return x * 0x2545F4914F6CDD1DULL;
+}
+static double orc_xs_in(uint64_t* st, double lo, double hi) {            /* rng.hpp:28-33 */
+    const double u = (double)(orc_xs_next(st) >> 11) * 0x1.0p-53;
+    return lo + (hi - lo) * u;
+}
+
+int orc_gen_packing(uint64_t n, double s, double jit, int poly, uint64_t seed, double omega_half,
+                    uint32_t* ids, double* pos, double* vel, double* omg, double* rad, double* mass,
+                    uint32_t* mat, double domain_max[3]) {
+    const double r0 = 0.005, m0 = 1e-3, r_max = r0;
+    const uint64_t side = (uint64_t)ceil(cbrt((double)n));
+    const double spacing = s * r0;
+    uint64_t st = seed != 0 ? seed : 0x9E3779B97F4A7C15ULL;              /* rng.hpp:13-15 */
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t ix = i % side, iy = (i / side) % side, iz = i / (side * side);
+        const double jx = orc_xs_in(&st, -jit * r0, jit * r0);
+        const double jy = orc_xs_in(&st, -jit * r0, jit * r0);
+        const double jz = orc_xs_in(&st, -jit * r0, jit * r0);
+        double r = r0, m = m0;
+        if (poly) {
+            r = r0 * orc_xs_in(&st, 0.5, 1.0);
+            const double q = r / r0;
+            m = m0 * q * q * q;
+        }
+        ids[i] = (uint32_t)i;
+        pos[3 * i + 0] = 2.0 * r_max + (double)ix * spacing + jx;
+        pos[3 * i + 1] = 2.0 * r_max + (double)iy * spacing + jy;
+        pos[3 * i + 2] = 2.0 * r_max + (double)iz * spacing + jz;
+        for (int a = 0; a < 3; ++a) vel[3 * i + a] = orc_xs_in(&st, -0.5, 0.5);
+        for (int a = 0; a < 3; ++a) omg[3 * i + a] = orc_xs_in(&st, -omega_half, omega_half);
+        rad[i] = r;
+        mass[i] = m;
+        mat[i] = 0;
+    }
+    domain_max[0] = domain_max[1] = domain_max[2] = (double)side * spacing + 4.0 * r_max;
+    return 0;
+}

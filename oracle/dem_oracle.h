@@ -165,6 +165,11 @@ void orc_sim_get_grid(const orc_sim* s, orc_grid* g);
 /* periodic box of a simulation: cell extents per axis and the current Lees-Edwards offset */
 void orc_sim_get_pbox(const orc_sim* s, double cell_extent[3], double* shear_offset, int64_t* shear_steps);
 
+/* bench input generator G(N, s, jit, poly, seed) of SURVEY.md §8d (bench_support.hpp:10-44, rng.hpp) */
+int orc_gen_packing(uint64_t n, double s, double jit, int poly, uint64_t seed, double omega_half,
+                    uint32_t* ids, double* pos, double* vel, double* omg, double* rad, double* mass,
+                    uint32_t* mat, double domain_max[3]);
+
 #ifdef __cplusplus
 }
 #endif

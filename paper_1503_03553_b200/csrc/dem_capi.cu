@@ -74,7 +74,8 @@ struct dem_ctx {
     uint64_t phase_count = 0;  // force phases executed (parity selects buffers)
     uint64_t replaced_at = ~0ull;  // phase_count when dem_set_particles last replaced the state
     bool state_invalid = false;     // the last upload was rejected (REQUIRE_STATE)
-    std::vector<uint32_t> checked_ids;  // the ids last checked unique (check_unique_ids)
+    uint32_t* idmap = nullptr;      // duplicate-id screen of uploads (upload_state), idmask + 1 bits
+    uint32_t idmask = 0;
     int64_t step_index = 0;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     cudaGraphExec_t graph_async[2] = {nullptr, nullptr};  // + the state-ready event node (dem_step_async)
@@ -484,6 +485,7 @@ void free_ctx(dem_ctx* c) {
     if (c->h_counters) cudaFreeHost(c->h_counters);
     if (c->raw_d) cudaFree(c->raw_d);
     if (c->raw_u) cudaFree(c->raw_u);
+    if (c->idmap) cudaFree(c->idmap);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -581,6 +583,12 @@ int ensure_raw(dem_ctx* ctx, uint64_t n) {
     if (ctx->raw_d) { cudaFree(ctx->raw_d); cudaFree(ctx->raw_u); ctx->raw_d = nullptr; ctx->raw_u = nullptr; }
     CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&ctx->raw_d), std::max<uint64_t>(n, 1) * 11 * sizeof(double)));
     CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&ctx->raw_u), std::max<uint64_t>(n, 1) * 2 * sizeof(uint32_t)));
+    uint64_t bits = 1024;
+    while (bits < 4 * n && bits < (1ull << 32)) bits <<= 1;
+    if (ctx->idmap) cudaFree(ctx->idmap);
+    ctx->idmap = nullptr;
+    CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&ctx->idmap), bits / 8));
+    ctx->idmask = static_cast<uint32_t>(bits - 1);
     ctx->raw_n = n;
     return DEM_OK;
 }
@@ -595,6 +603,25 @@ RawState raw_view(const dem_ctx* ctx, uint64_t n) {
     r.ids = ctx->raw_u;
     r.mat = ctx->raw_u + n;
     return r;
+}
+
+// ParticleSet ids must be unique for the B200 path: its contact history is keyed by the partner's
+// stable id (the reference keys it by slot, contact_table.hpp:16-24). Exact, O(n log n) on a copy:
+// at creation, and after an upload whose device screen saw a possible duplicate (upload_state).
+int check_unique_ids(const uint32_t* ids, uint64_t n, std::string* why) {
+    if (!ids) return DEM_OK;
+    std::vector<uint32_t> v(ids, ids + n);
+    std::sort(v.begin(), v.end());
+    const auto d = std::adjacent_find(v.begin(), v.end());
+    if (d != v.end()) {
+        *why = "particle " + std::to_string(*d) + ": duplicate stable id (the B200 contact history is keyed by id)";
+        return DEM_ERR_CONFIG;
+    }
+    if (n && v.back() > 0xFFFFFFBFu) {
+        *why = "particle " + std::to_string(v.back()) + ": stable id in the reserved wall-key range (>= 0xFFFFFFC0)";
+        return DEM_ERR_CONFIG;
+    }
+    return DEM_OK;
 }
 
 // Host arrays -> device staging (plain copies; pinned callers get full PCIe bandwidth) -> SoA.
@@ -625,13 +652,28 @@ int upload_state(dem_ctx* ctx, const dem_particles* p, int buf) {
     // every packed particle is validated on the device as it is packed (ParticleSet::validate,
     // particle_set.cpp:40-58; material ids < count, since they index the force kernel's shared
     // material table; stable ids below the wall keys): free for the host-coupled stepping loop
+    // Duplicate ids are screened on the device too: the ids hash into a bitmap of >= 4n bits
+    // (id mod 2^k: a permutation of 0..n-1, the usual ids, never collides); only a collision
+    // sends the ids through the exact host check.
     CUDA_TRY(cudaMemsetAsync(&ctx->ctl->bad_upload, 0xff, sizeof(unsigned long long), s));
-    launch_pack_state(ctx->state[buf], r, static_cast<uint32_t>(n), true, s, ctx->ctl,
-                      static_cast<uint32_t>(ctx->materials.size()), r.rad && r.mass ? &ctx->ctl->r_ref : nullptr);
-    unsigned long long bad = ~0ull;
-    CUDA_TRY(cudaMemcpyAsync(&bad, &ctx->ctl->bad_upload, sizeof(bad), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemsetAsync(&ctx->ctl->maybe_dup, 0, sizeof(unsigned int), s));
+    if (r.ids) CUDA_TRY(cudaMemsetAsync(ctx->idmap, 0, (static_cast<size_t>(ctx->idmask) + 1) / 8, s));
+    const PackCheck chk{ctx->ctl, static_cast<uint32_t>(ctx->materials.size()), r.ids ? ctx->idmap : nullptr, ctx->idmask};
+    launch_pack_state(ctx->state[buf], r, static_cast<uint32_t>(n), true, s, &chk,
+                      r.rad && r.mass ? &ctx->ctl->r_ref : nullptr);
+    struct { unsigned long long bad; unsigned int dup; } flags{~0ull, 0u};
+    CUDA_TRY(cudaMemcpyAsync(&flags.bad, &ctx->ctl->bad_upload, sizeof(flags.bad), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(&flags.dup, &ctx->ctl->maybe_dup, sizeof(flags.dup), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     CUDA_TRY(cudaGetLastError());
+    const unsigned long long bad = flags.bad;
+    if (bad == ~0ull && flags.dup) {
+        std::string why;
+        if (check_unique_ids(p->ids, n, &why) != DEM_OK) {
+            ctx->state_invalid = true;
+            return set_error(ctx, DEM_ERR_CONFIG, -1, 0, 0, ctx->step_index, why);
+        }
+    }
     if (bad != ~0ull) {
         // the buffer now holds the rejected particles: no phase may run on it until a valid upload
         ctx->state_invalid = true;
@@ -647,27 +689,6 @@ int upload_state(dem_ctx* ctx, const dem_particles* p, int buf) {
     return DEM_OK;
 }
 
-// ParticleSet ids must be unique for the B200 path: its contact history is keyed by the partner's
-// stable id (the reference keys it by slot, contact_table.hpp:16-24). O(n log n) on a copy; a
-// re-upload of the ids last checked skips the sort (one memcmp).
-int check_unique_ids(const uint32_t* ids, uint64_t n, std::vector<uint32_t>* cache, std::string* why) {
-    if (!ids) return DEM_OK;
-    if (cache && cache->size() == n && (n == 0 || std::memcmp(cache->data(), ids, n * sizeof(uint32_t)) == 0))
-        return DEM_OK;
-    std::vector<uint32_t> v(ids, ids + n);
-    std::sort(v.begin(), v.end());
-    const auto d = std::adjacent_find(v.begin(), v.end());
-    if (d != v.end()) {
-        *why = "particle " + std::to_string(*d) + ": duplicate stable id (the B200 contact history is keyed by id)";
-        return DEM_ERR_CONFIG;
-    }
-    if (n && v.back() > 0xFFFFFFBFu) {
-        *why = "particle " + std::to_string(v.back()) + ": stable id in the reserved wall-key range (>= 0xFFFFFFC0)";
-        return DEM_ERR_CONFIG;
-    }
-    if (cache) cache->assign(ids, ids + n);
-    return DEM_OK;
-}
 
 int run_phase(dem_ctx* ctx, uint32_t flags, dem_step_metrics* m, bool is_step) {
     if (ctx->n == 0) {
@@ -703,7 +724,7 @@ int dem_create(const dem_config* cfg, const dem_particles* particles, int device
     *out = nullptr;
     std::string why;
     int rc = validate(cfg, particles, &why);
-    if (rc == DEM_OK) rc = check_unique_ids(particles->ids, particles->count, nullptr, &why);
+    if (rc == DEM_OK) rc = check_unique_ids(particles->ids, particles->count, &why);
     if (rc != DEM_OK) {
         std::snprintf(g_create_error.message, sizeof(g_create_error.message), "%s", why.c_str());
         g_create_error.code = rc;
@@ -829,7 +850,6 @@ int dem_clone(const dem_ctx* src, dem_ctx** out) {
     ctx->phase_count = src->phase_count;
     ctx->replaced_at = src->replaced_at;
     ctx->state_invalid = src->state_invalid;
-    ctx->checked_ids = src->checked_ids;
     ctx->step_index = src->step_index;
     ctx->last_error = src->last_error;
     if (rc == DEM_OK) rc = build_graphs(ctx);
@@ -953,9 +973,6 @@ int dem_set_particles(dem_ctx* ctx, const dem_particles* in) {
     if (!in->positions || !in->velocities || !in->angular_velocities) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
     SETTLE(ctx);
-    std::string why;
-    if (check_unique_ids(in->ids, in->count, &ctx->checked_ids, &why) != DEM_OK)
-        return set_error(ctx, DEM_ERR_CONFIG, -1, 0, 0, ctx->step_index, why);
     ctx->replaced_at = ctx->phase_count;  // the binning no longer matches the state (traces)
     return upload_state(ctx, in, state_cur(ctx));
 }

@@ -78,6 +78,7 @@ struct DevCtl {
     long long le_steps;                         // integrating phases so far (Lees-Edwards clock)
     double le_delta;                            // Lees-Edwards image offset of the upper box
     unsigned long long bad_upload;              // (slot<<8)|reason of the first invalid uploaded particle, atomicMin
+    unsigned int maybe_dup;                     // an uploaded id hashed onto an occupied idmap bit
 };
 
 // Structure-of-arrays particle state for one buffer (sorted slot order).
@@ -177,11 +178,19 @@ struct RawState {
     double *pos, *vel, *omg, *rad, *mass;
     uint32_t *ids, *mat;
 };
-// pack: host layout -> SoA, and (ref non-null) ref[0], ref[1] = particle 0's radius and mass; with
-// `check`, every packed particle is validated (ParticleSet::validate, particle_set.cpp:40-58, plus
-// the B200 id range) and the first invalid slot lands in check->bad_upload
+// Upload validation done by the pack kernel (ParticleSet::validate, particle_set.cpp:40-58, plus
+// the B200 id rules): the first invalid slot lands in ctl->bad_upload; uploaded ids are hashed into
+// idmap (a bitmap of idmask + 1 bits, zeroed by the caller) and a set bit already present raises
+// ctl->maybe_dup (a duplicate id, or a hash collision the host then resolves exactly).
+struct PackCheck {
+    DevCtl* ctl;
+    uint32_t nmat;
+    uint32_t* idmap;   // nullptr: ids not uploaded (kept), no duplicate screen
+    uint32_t idmask;
+};
+// pack: host layout -> SoA, and (ref non-null) ref[0], ref[1] = particle 0's radius and mass
 void launch_pack_state(const StateBuf& s, const RawState& r, uint32_t n, bool pack, cudaStream_t st,
-                       DevCtl* check = nullptr, uint32_t nmat = 0, double* ref = nullptr);
+                       const PackCheck* check = nullptr, double* ref = nullptr);
 void launch_ft_layout(double* ft, uint32_t stride, double* f, double* t, uint32_t n, bool to_interleaved, cudaStream_t st);
 cudaError_t init_device_attributes();
 

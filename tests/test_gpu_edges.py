@@ -150,11 +150,20 @@ def test_set_particles_validates_on_device(cuda):
             sim.step()
         sim.set_particles(good)
         sim.step()
+    # duplicates: screened on the device by an id bitmap, confirmed exactly on the host
     dup = good.copy()
     dup.ids[3] = dup.ids[4]
     with pytest.raises(dem.ConfigError, match="duplicate"):
         sim.set_particles(dup)
-    sim.step()  # rejected on the host before any upload: the state is untouched
+    with pytest.raises(dem.ConfigError):
+        sim.step()
+    # a hash collision that is no duplicate (ids equal modulo the bitmap size) is accepted
+    far = good.copy()
+    far.ids[5] = far.ids[6] + (1 << 20)
+    sim.set_particles(far)
+    sim.step()
+    sim.set_particles(good)
+    sim.step()
     # particles_into checks the caller's arrays before writing through their pointers
     out = dem.ParticleSet(64)
     out.positions = np.zeros((64, 3), np.float32)

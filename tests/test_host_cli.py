@@ -81,6 +81,10 @@ def test_cli_verify_and_bench(cuda):
         print(r.stdout)
         assert r.returncode == 0, r.stdout + r.stderr
         assert r.stdout.count("PASS") == 5
+        # the reference's five property names (runner.cpp:274-417), incl. the independent oracle
+        for name in ("contact-completeness", "force-oracle-equivalence", "friction-bound",
+                     "momentum-conservation", "energy-dissipation"):
+            assert f"PASS  {name}:" in r.stdout, name
         r = subprocess.run([CLI, "bench", os.path.join(ROOT, "configs", "settle512.cfg"), "--steps", "5",
                             "--out-dir", d], capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr

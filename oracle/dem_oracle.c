@@ -590,6 +590,7 @@ struct orc_sim {
     size_t n;
     uint32_t *ids, *mat, *keys;
     double *pos, *vel, *omg, *rad, *mass, *F, *Tq;
+    double *Fabs, *Tabs; /* per particle: sum of |contribution| (the 1e-9 parity scale) */
     orc_hist* hist; int64_t nhist, hcap;
     int64_t step_index, clamps;
     /* per-particle counters for metrics */
@@ -645,6 +646,8 @@ static int apply_contact(orc_sim* s, size_t i, const double g[10], uint32_t mi, 
     orc_contact_force(g, co, dt_, mu, s->rad[i], f);
     st3(s->F + 3 * i, add(ld3(s->F + 3 * i), ld3(f)));
     st3(s->Tq + 3 * i, add(ld3(s->Tq + 3 * i), ld3(f + 3)));
+    s->Fabs[i] += norm(ld3(f));
+    s->Tabs[i] += norm(ld3(f + 3));
     if (wall) ++s->wall_count[i]; else ++s->pp_count[i];
     const double limit = mu * f[9];
     if (limit > 0.0) {
@@ -710,9 +713,14 @@ int orc_sim_force_phase(orc_sim* s, int flags, orc_metrics* m, orc_error* err) {
     /* zero_forces + ForceGravity, pipeline.cpp:137-139, 46-50 */
     memset(s->F, 0, 3 * n * sizeof(double));
     memset(s->Tq, 0, 3 * n * sizeof(double));
+    memset(s->Fabs, 0, n * sizeof(double));
+    memset(s->Tabs, 0, n * sizeof(double));
     if (flags & ORC_PH_GRAVITY) {
         const v3 g = ld3(s->g);
-        for (size_t i = 0; i < n; ++i) st3(s->F + 3 * i, add(ld3(s->F + 3 * i), muls(g, s->mass[i])));
+        for (size_t i = 0; i < n; ++i) {
+            st3(s->F + 3 * i, add(ld3(s->F + 3 * i), muls(g, s->mass[i])));
+            s->Fabs[i] = norm(muls(g, s->mass[i]));
+        }
     }
     /* InitializeContactIDs (sweep): the live entries are exactly the previous phase's touched
      * ones, which is what s->hist holds (contact_table.cpp:37-46). */
@@ -912,6 +920,8 @@ orc_sim* orc_sim_create(const orc_config* cfg, size_t n, const uint32_t* ids, co
     s->keys = (uint32_t*)calloc(n + 1, sizeof(uint32_t));
     s->F = (double*)calloc(3 * n + 1, sizeof(double));
     s->Tq = (double*)calloc(3 * n + 1, sizeof(double));
+    s->Fabs = (double*)calloc(n + 1, sizeof(double));
+    s->Tabs = (double*)calloc(n + 1, sizeof(double));
     s->pp_count = (uint32_t*)calloc(n + 1, sizeof(uint32_t));
     s->wall_count = (uint32_t*)calloc(n + 1, sizeof(uint32_t));
     s->fric = (double*)calloc(n + 1, sizeof(double));
@@ -964,7 +974,7 @@ void orc_sim_destroy(orc_sim* s) {
     if (!s) return;
     free_tables(&s->T); free(s->rects); free(s->lines);
     free(s->ids); free(s->mat); free(s->keys); free(s->pos); free(s->vel); free(s->omg);
-    free(s->rad); free(s->mass); free(s->F); free(s->Tq); free(s->hist);
+    free(s->rad); free(s->mass); free(s->F); free(s->Tq); free(s->Fabs); free(s->Tabs); free(s->hist);
     free(s->pp_count); free(s->wall_count); free(s->fric); free(s->cstart); free(s->cend);
     free(s);
 }
@@ -993,6 +1003,10 @@ void orc_sim_get_state(const orc_sim* s, uint32_t* ids, double* pos, double* vel
 void orc_sim_get_forces(const orc_sim* s, double* f, double* t) {
     if (f) memcpy(f, s->F, 3 * s->n * sizeof(double));
     if (t) memcpy(t, s->Tq, 3 * s->n * sizeof(double));
+}
+void orc_sim_get_force_scale(const orc_sim* s, double* fabs_, double* tabs_) {
+    memcpy(fabs_, s->Fabs, s->n * sizeof(double));
+    memcpy(tabs_, s->Tabs, s->n * sizeof(double));
 }
 void orc_sim_get_keys(const orc_sim* s, uint32_t* k) { memcpy(k, s->keys, s->n * sizeof(uint32_t)); }
 int64_t orc_sim_history_count(const orc_sim* s) { return s->nhist; }

@@ -159,6 +159,9 @@ void orc_sim_get_state(const orc_sim* s, uint32_t* ids, double* pos, double* vel
                        double* rad, double* mass, uint32_t* mat);
 void orc_sim_get_forces(const orc_sim* s, double* forces, double* torques);
 void orc_sim_get_keys(const orc_sim* s, uint32_t* sorted_keys);
+/* per slot, the last phase's sum of |F| and |T| contributions (gravity, contacts, walls): the scale
+ * of the 1e-9 relative parity criterion (SURVEY §8a notes) */
+void orc_sim_get_force_scale(const orc_sim* s, double* f_abs, double* t_abs);
 int64_t orc_sim_history_count(const orc_sim* s);
 void orc_sim_get_history(const orc_sim* s, orc_hist* out);
 void orc_sim_get_grid(const orc_sim* s, orc_grid* g);

@@ -191,6 +191,7 @@ class Oracle:
         L.orc_sim_get_state.argtypes = [C.c_void_p, PU, PD, PD, PD, PD, PD, PU]
         L.orc_sim_get_forces.argtypes = [C.c_void_p, PD, PD]
         L.orc_sim_get_keys.argtypes = [C.c_void_p, PU]
+        L.orc_sim_get_force_scale.argtypes = [C.c_void_p, PD, PD]
         L.orc_sim_history_count.restype = C.c_int64
         L.orc_sim_history_count.argtypes = [C.c_void_p]
         L.orc_sim_get_history.argtypes = [C.c_void_p, C.POINTER(orc_hist)]
@@ -355,6 +356,13 @@ class OracleSim:
         f = np.zeros((self.n, 3))
         t = np.zeros((self.n, 3))
         self.o.L.orc_sim_get_forces(self.h, f.ctypes.data_as(PD), t.ctypes.data_as(PD))
+        return f, t
+
+    def force_scale(self):
+        """Per slot: sum of |F| and of |T| contributions of the last phase (SURVEY §8a's 1e-9 scale)."""
+        f = np.zeros(self.n)
+        t = np.zeros(self.n)
+        self.o.L.orc_sim_get_force_scale(self.h, f.ctypes.data_as(PD), t.ctypes.data_as(PD))
         return f, t
 
     def keys(self):

@@ -430,7 +430,8 @@ int collect(dem_ctx* ctx, dem_step_metrics* m, uint64_t phase_before, int64_t st
         clean.err_key = kNoError;
         for (auto& s : clean.err_sid) s = kNoError;
         clean.halted = 0;
-        CUDA_TRY(cudaMemcpy(ctx->ctl, &clean, sizeof(DevCtl), cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpyAsync(ctx->ctl, &clean, sizeof(DevCtl), cudaMemcpyHostToDevice, ctx->stream));
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         return code;
     }
     if (m) {
@@ -682,8 +683,10 @@ int upload_state(dem_ctx* ctx, const dem_particles* p, int buf) {
                                           "bad material", "stable id in the reserved wall-key range (>= 0xFFFFFFC0)"};
         const uint32_t code = static_cast<uint32_t>(bad & 0xff);
         const uint32_t id = p->ids ? p->ids[slot] : 0u;
+        char raw[64];
+        std::snprintf(raw, sizeof(raw), " (slot %llu, check word 0x%llx)", static_cast<unsigned long long>(slot), bad);
         return set_error(ctx, DEM_ERR_CONFIG, -1, static_cast<uint32_t>(slot), id, ctx->step_index,
-                         "particle " + std::to_string(id) + ": " + why[code < 6 ? code : 0]);
+                         "particle " + std::to_string(id) + ": " + why[code < 6 ? code : 0] + (code < 6 && code ? "" : raw));
     }
     ctx->state_invalid = false;
     return DEM_OK;
@@ -777,7 +780,11 @@ int dem_create(const dem_config* cfg, const dem_particles* particles, int device
         DevCtl init{};
         init.err_key = kNoError;
         for (auto& s : init.err_sid) s = kNoError;
-        if (cudaMemcpy(ctx->ctl, &init, sizeof(DevCtl), cudaMemcpyHostToDevice) != cudaSuccess) rc = DEM_ERR_CUDA;
+        // on the context's stream: a legacy cudaMemcpy from pageable memory may complete its DMA after
+        // later work on this non-blocking stream (upload_state's check-word reset)
+        if (cudaMemcpyAsync(ctx->ctl, &init, sizeof(DevCtl), cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
+            cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+            rc = DEM_ERR_CUDA;
     }
     if (rc == DEM_OK) rc = upload_state(ctx, particles, 0);
     if (rc == DEM_OK) rc = build_graphs(ctx);
@@ -1078,11 +1085,14 @@ int dem_set_contacts(dem_ctx* ctx, const uint32_t* owner_slot, const int32_t* pa
         for (int a = 0; a < 3; ++a) dt[a * cap + q] = delta_t[3 * k + a];
     }
     const HistBuf& h = ctx->hist[hist_cur(ctx)];
-    CUDA_TRY(cudaMemcpy(h.pos, pos.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(h.cnt, cnt.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(h.key, key.data(), cap * sizeof(uint32_t), cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(h.dt, dt.data(), 3 * cap * sizeof(double), cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(ctx->pair_j, pj.data(), cap * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    // on the context's (non-blocking) stream, so the next phase is ordered after the DMA
+    cudaStream_t st = ctx->stream;
+    CUDA_TRY(cudaMemcpyAsync(h.pos, pos.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(h.cnt, cnt.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(h.key, key.data(), cap * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(h.dt, dt.data(), 3 * cap * sizeof(double), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(ctx->pair_j, pj.data(), cap * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
     return DEM_OK;
 }
 
@@ -1338,7 +1348,11 @@ int dem_create_slab(const dem_config* cfg, const dem_particles* owned, int devic
         DevCtl init{};
         init.err_key = kNoError;
         for (auto& s : init.err_sid) s = kNoError;
-        if (cudaMemcpy(ctx->ctl, &init, sizeof(DevCtl), cudaMemcpyHostToDevice) != cudaSuccess) rc = DEM_ERR_CUDA;
+        // on the context's stream: a legacy cudaMemcpy from pageable memory may complete its DMA after
+        // later work on this non-blocking stream (upload_state's check-word reset)
+        if (cudaMemcpyAsync(ctx->ctl, &init, sizeof(DevCtl), cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
+            cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+            rc = DEM_ERR_CUDA;
     }
     if (rc == DEM_OK) rc = upload_state(ctx, owned, 0);
     if (rc != DEM_OK) {

@@ -220,13 +220,14 @@ def cpu_reference_run(ps, cfg, steps, warmup, budget_s, threads=None):
     return {"value": value, "steps": done, "seconds": t_total, "cores": cores, "ctor_s": t_ctor}
 
 
-def cpu_baseline_block(ps, cfg, steps, warmup, budget_s):
+def cpu_baseline_block(ps, cfg, steps, warmup, budget_s, sample="262,144-particle"):
     """All host threads, then one thread (both, with the CPU model and core count)."""
     info = host_info()
     r = cpu_reference_run(ps, cfg, steps, warmup, budget_s)
-    r1 = cpu_reference_run(ps, cfg, 3, 0, float(os.environ.get("DEM_CPU1_BUDGET_S", "10")), threads=1)
+    r1 = cpu_reference_run(ps, cfg, 3 if len(ps.ids) <= 1 << 20 else 1, 0,
+                           float(os.environ.get("DEM_CPU1_BUDGET_S", "10")), threads=1)
     block = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "reference",
-             "sample": f"{r['steps']} full steps of the same 262,144-particle workload "
+             "sample": f"{r['steps']} full steps of the same {sample} workload "
                        f"({r['seconds']:.1f} s) through the reference Simulation::step() compiled from "
                        f"its sources (oracle/_ref), DEMFORGE threads={r['cores']}",
              "threads1": {"value": r1["value"], "unit": UNIT, "cores": 1,
@@ -242,8 +243,18 @@ def run_reference(args):
     world, rank, local = dist_env()
     if rank != 0:
         return 0
-    ps, cfg = reference_workload()
-    r, block = cpu_baseline_block(ps, cfg, args.steps, args.warmup, float("inf"))
+    if world == 1:
+        ps, cfg = reference_workload()
+        sample = "262,144-particle"
+    else:
+        # configs[3]'s 8M packing; the reference has no periodic box or shear, so it
+        # runs the walled proxy of the same packing
+        from oracle.workload import gen_packing, packing_config
+        ps, dmax = gen_packing(N_CONFIG3, s=1.8, jit=0.2, poly=False, seed=4)
+        cfg = packing_config(dmax)
+        sample = "8,388,608-particle (walled proxy of configs[3])"
+    r, block = cpu_baseline_block(ps, cfg, args.steps, args.warmup,
+                                  float(os.environ.get("DEM_REF_BUDGET_S", "900")), sample)
     line = {
         "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
         "n_gpus": args.gpus, "steps": r["steps"], "warmup": args.warmup,
@@ -258,99 +269,111 @@ def run_reference(args):
     return 0
 
 
+N_CONFIG3 = 8388608
+
+
 def slab_config(world):
-    """The N > 1 workload (identical in both arms)."""
-    n_total = N_PARTICLES * world
-    return {"workload": f"{n_total:,} monodisperse spheres, dense packing = configs[1] per GPU",
-            "generator": f"G({n_total}, s=1.8, jit=0.2, mono, seed=1)", "dt": 1e-5,
-            "contact_capacity": 16, "parallelism": f"z-slabs x{world}",
-            "l2": "flushed before every timed step, outside the events"}
+    """The N > 1 workload (identical in both arms): BASELINE configs[3], 8M spheres in a periodic
+    Lees-Edwards shear box, z-slabs over the N GPUs (strong scaling: the total is fixed)."""
+    return {"workload": "8,388,608 monodisperse spheres in a periodic Lees-Edwards shear box (configs[3])",
+            "generator": "G(8388608, s=1.8, jit=0.2, mono, seed=4), periodic x/y/z, shear rate 1/s (flow x, gradient y)",
+            "dt": 1e-5, "contact_capacity": 16, "parallelism": f"z-slabs x{world}, host-free sharded step",
+            "l2": "inputs larger than L2 (>= 0.4 GB of particle state per GPU), no flush"}
 
 
-def run_slab(args, world, rank, local):
-    """N > 1: one packing of 262,144 x N spheres, cut into N z-slabs (weak scaling), one slab
-    per GPU; neighbour migrant/halo records stored into the neighbours' memory by the pack
-    kernels (CUDA IPC over NVLink), counts over gloo (paper_1503_03553_b200.slab.PeerTransport)."""
+def run_sharded(args, world, rank, local):
+    """N > 1: BASELINE configs[3] over N GPUs with the host-free sharded step (dem_create_sharded):
+    one process per GPU, the neighbours' inboxes opened through CUDA IPC (NVLink peer memory),
+    counts on the device, each step one CUDA graph. value = 8,388,608 x K / max over ranks of the
+    summed per-step device times (CUDA events on each rank's stream)."""
     import torch
     import torch.distributed as dist
     import paper_1503_03553_b200 as dem
-    from paper_1503_03553_b200.slab import PeerTransport, SlabDriver, TorchTransport, build_local_slabs
-    n_total = N_PARTICLES * world
-    ps, dmax = dem.gen_packing(n_total, s=1.8, jit=0.2, poly=False, seed=1)
-    cfg = dem.packing_config(dmax)
-    ranks, bounds, g = build_local_slabs(ps, cfg, world, [rank], device=local)
-    # records through NVLink peer memory (pack kernels store into the neighbours' buffers); NCCL
-    # point-to-point messages if IPC peer access is unavailable on this box
-    transport = "peer"
-    try:
-        tr = PeerTransport(rank, world)
-        tr.bind(ranks[0])
-    except Exception:  # noqa: BLE001
-        transport = "nccl"
-        tr = TorchTransport(rank, world)
-        tr.bind(ranks[0])
-    drv = SlabDriver(ranks, tr)
-    drv.prime()
-    for _ in range(args.warmup):
-        drv.step()
-    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
-    step_ms, contacts = [], 0
+    from paper_1503_03553_b200.slab import ShardedSimulation, connect_torch
+    ps, L = dem.gen_periodic_packing(N_CONFIG3, s=1.8, jit=0.2, seed=4)
+    cfg = dem.periodic_config(L, shear_rate=1.0)
+    sim = ShardedSimulation(ps, cfg, rank, world, device=local)
+    del ps
+    connect_torch(sim)
+    for _ in range(max(1, args.warmup)):
+        sim.step()
     barrier(world)
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        for k in range(args.steps):
-            flush.fill_(k)  # evict L2 outside the timed events
-            torch.cuda.synchronize()
-            barrier(world)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            ms = drv.step()  # host-orchestrated: slab kernels + NCCL P2P + force phase, synced
-            e1.record()
-            torch.cuda.synchronize()
-            step_ms.append(e0.elapsed_time(e1))
-            contacts = ms[0].contacts
+        step_ms, m = sim.time_steps(args.steps, 0)
     barrier(world)
     total_s = max_over_ranks(sum(step_ms) / 1e3, world)
-    c_all = torch.tensor([contacts], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
-    dist.all_reduce(c_all)
-    value = n_total * args.steps / total_s
-    # e2e: the same stepping with every rank reading its slab's particle state (owned + halo
-    # slots, dem_get_particles) back into pinned host memory each step
+    value = N_CONFIG3 * args.steps / total_s
+    contacts = max_over_ranks(float(m.contacts), world)  # per-rank; reported for the slowest rank
+    z_lo, z_hi, owned = sim.info()
+    # e2e: the same steps through the public API (dem_step) with every rank reading its slab's
+    # state back into pinned host memory after each step, wall clock, max over ranks
+    host = pinned_particles(int(sim.size()) + 4096)
     import ctypes as C
-    host = pinned_particles(2 * int(ranks[0].lib.dem_size(ranks[0].ctx)) + 1024)
     t_e2e, d2h = [], 0
-    for it in range(max(3, min(args.steps, 10)) + 1):  # iteration 0: untimed (staging allocation)
-        torch.cuda.synchronize()
+    e2e_steps = max(3, min(args.steps, 10))
+    for _ in range(e2e_steps):
+        barrier(world)
         t0 = time.perf_counter()
-        drv.step()
-        n_loc = int(ranks[0].lib.dem_size(ranks[0].ctx))
+        sim.step()
+        n_loc = sim.size()
         view = dem.ParticleSet(0)
         for f in ("ids", "positions", "velocities", "angular_velocities", "radii", "masses", "material_ids"):
             setattr(view, f, getattr(host, f)[:n_loc])
-        rc = ranks[0].lib.dem_get_particles(ranks[0].ctx, C.byref(view.c_struct()))
+        rc = sim.lib.dem_get_particles(sim.ctx, C.byref(view.c_struct()))
         assert rc == 0, rc
-        if it:
-            t_e2e.append(time.perf_counter() - t0)
-            d2h += n_loc * 96
+        t_e2e.append(time.perf_counter() - t0)
+        d2h += n_loc * 96
     e2e_s = max_over_ranks(sum(t_e2e), world)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (SURVEY §8d generator, xorshift64*)",
         "config": slab_config(world),
-        "workload_stats": {"contacts_per_step": int(c_all.item()), "slabs": bounds,
-                           "transport": "NVLink peer-memory stores (CUDA IPC)" if transport == "peer" else "NCCL P2P"},
-        "gpu_launches": 11 * args.steps,
-        "e2e": {"value": n_total * len(t_e2e) / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": int(d2h / len(t_e2e)),
-                "how": "slab step + per-rank state readback into pinned host memory (dem_get_particles), wall clock"},
+        "workload_stats": {"particles": N_CONFIG3, "box_length": L, "rank0_slab_planes": [z_lo, z_hi],
+                           "rank0_owned": owned, "contacts_per_step_max_rank": contacts},
+        "gpu_launches": 16 * args.steps,
+        "e2e": {"value": N_CONFIG3 * e2e_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": int(d2h / e2e_steps),
+                "how": "dem_step (host-free sharded step) + per-rank dem_get_particles of the slab into pinned host memory, wall clock, max over ranks"},
         "clocks": clk.summary(),
     }
+    del sim
+    if world > 1 and not args.no_north_star:
+        barrier(world)
+        line["north_star_32m"] = north_star_sharded(args, world, rank, local)
+    barrier(world)
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
     return 0
+
+
+def north_star_sharded(args, world, rank, local):
+    """north_star's target on N GPUs: 32M dense frictional spheres, walled box, z-slabs."""
+    import torch
+    import paper_1503_03553_b200 as dem
+    from paper_1503_03553_b200.slab import ShardedSimulation, connect_torch
+    n = 1 << 25
+    ps, dmax = dem.gen_packing(n, s=1.8, jit=0.2, poly=False, seed=5)
+    sim = ShardedSimulation(ps, dem.packing_config(dmax), rank, world, device=local)
+    del ps
+    connect_torch(sim)
+    for _ in range(3):
+        sim.step()
+    steps = max(3, min(args.steps, 10))
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        step_ms, m = sim.time_steps(steps, 0)
+    total_s = max_over_ranks(sum(step_ms) / 1e3, world)
+    del sim
+    return {"workload": "33,554,432 monodisperse spheres, dense frictional packing (north_star target)",
+            "generator": "G(33554432, s=1.8, jit=0.2, mono, seed=5)", "dtype": "f64", "contact_capacity": 16,
+            "value": n * steps / total_s, "unit": UNIT, "steps": steps, "warmup": 3,
+            "ms_per_step": 1e3 * total_s / steps, "scaling": "strong", "clocks": clk.summary(),
+            "l2": "inputs larger than L2, no flush"}
 
 
 def north_star_block(args):
@@ -404,7 +427,7 @@ def run_b200(args):
             local = local % ngpu
             torch.cuda.set_device(local)
             dist.init_process_group("gloo")
-        return run_slab(args, world, rank, local)
+        return run_sharded(args, world, rank, local)
     torch.cuda.set_device(0)
     import paper_1503_03553_b200 as dem
 

@@ -307,6 +307,41 @@ int dem_ipc_handle(int device, void* ptr, void* handle64);
 int dem_ipc_open(int device, const void* handle64, void** ptr);
 int dem_ipc_close(int device, void* ptr);
 
+/* ---- host-free sharded stepping: the multi-GPU Simulation (SURVEY §8b "dem_create_sharded";
+ * §8e). Replaces, for N GPUs, the reference's single-process Simulation(ParticleSet, SimConfig)
+ * (pipeline.hpp:64) + step() (:68); no reference counterpart for the decomposition itself
+ * (SPEC.md:382-383 lists multi-node as a non-goal).
+ *
+ *   dem_create_sharded(cfg, ALL particles, device, rank, nranks, &ctx)   every rank, same inputs:
+ *       rank `rank` keeps the z-slab of whole cell planes the deterministic, count-balanced
+ *       partition assigns it (plus a one-plane halo each step)
+ *   dem_shard_handle(ctx, handle64)        64 bytes: this rank's inbox (a CUDA IPC handle)
+ *   -- the caller all-gathers the nranks handles (ncclAllGather, MPI_Allgather, torch) --
+ *   dem_shard_connect(ctx, handles)        nranks * 64 bytes, rank order; opens the neighbours'
+ *                                          inboxes (one process per GPU, NVLink peer memory)
+ *   dem_shard_connect_local(ctx, lo, hi)   instead: contexts of ONE process (lo / hi = the
+ *                                          z-neighbours' contexts, NULL at a non-periodic edge)
+ *   dem_step(ctx, n, &m)                   n steps (the first call also runs the priming pass)
+ *
+ * A step is one CUDA graph with no host round trip: record counts stay on the device, the
+ * migrate / halo pack kernels store records and counts straight into the neighbours' inboxes and
+ * raise a flag (release store, system scope), and the stream waits for the neighbours' flags
+ * (stream memory operation; a spin kernel where unavailable). Every rank must step the same number
+ * of times: dem_step on ranks of one process would wait for each other, so there call
+ * dem_shard_launch on every rank, then dem_shard_wait on every rank. Results are bitwise identical
+ * to one context (canonical in-cell order). dem_get_particles / dem_get_forces / dem_get_contacts
+ * return the slab's slots, owned and halo: halo copies have material_ids bit 31 set.
+ * dem_time_steps times graph-launched steps (after a first dem_step). Tear-down: destroy every
+ * rank only after all ranks have finished stepping (their stores target each other's memory). */
+int dem_create_sharded(const dem_config* config, const dem_particles* all_particles, int device, int rank,
+                       int nranks, dem_ctx** out);
+int dem_shard_info(const dem_ctx* ctx, int32_t* z_lo, int32_t* z_hi, uint64_t* owned);
+int dem_shard_handle(const dem_ctx* ctx, void* handle64);
+int dem_shard_connect(dem_ctx* ctx, const void* handles);
+int dem_shard_connect_local(dem_ctx* ctx, dem_ctx* lo, dem_ctx* hi);
+int dem_shard_launch(dem_ctx* ctx, int nsteps);
+int dem_shard_wait(dem_ctx* ctx, dem_step_metrics* last);
+
 /* Diagnostics: the force kernel's shared-reciprocal division against the plain IEEE '/' on n
  * seeded random operand pairs (random bit patterns, exponents around the
  * fast-path bounds, contact-like magnitudes). *mismatches = results that differ in any bit. */

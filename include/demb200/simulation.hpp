@@ -422,6 +422,88 @@ inline void force_gravity(const ParticleSet& state, ForceAccumulator& forces, co
     }
 }
 
+namespace detail {
+
+// SimConfig -> dem_config (the arrays it points into live here)
+struct CConfig {
+    dem_config c{};
+    std::vector<dem_material> mats;
+    std::vector<double> pair;
+    std::vector<dem_rect_wall> rects;
+    std::vector<dem_line_wall> lines;
+
+    void build(const SimConfig& cfg) {
+        const auto m = cfg.materials.size();
+        mats.resize(m);
+        pair.resize(m * m);
+        for (std::size_t k = 0; k < m; ++k) {
+            const auto& q = cfg.materials.params(std::uint32_t(k));
+            mats[k] = dem_material{q.poisson_ratio, q.shear_modulus, q.youngs_modulus, q.restitution, q.sliding_friction};
+        }
+        for (std::size_t a = 0; a < m; ++a)
+            for (std::size_t b = 0; b < m; ++b) pair[a * m + b] = cfg.materials.pair_restitution(std::uint32_t(a), std::uint32_t(b));
+        rects.clear();
+        for (const auto& w : cfg.rect_walls)
+            rects.push_back(dem_rect_wall{{w.corner.x, w.corner.y, w.corner.z}, {w.edge_u.x, w.edge_u.y, w.edge_u.z},
+                                          {w.edge_v.x, w.edge_v.y, w.edge_v.z}, w.material_id});
+        lines.clear();
+        for (const auto& w : cfg.line_walls)
+            lines.push_back(dem_line_wall{{w.a.x, w.a.y, w.a.z}, {w.b.x, w.b.y, w.b.z}, w.material_id});
+        c = dem_config{};
+        c.dt = cfg.dt;
+        c.gravity[0] = cfg.gravity.x; c.gravity[1] = cfg.gravity.y; c.gravity[2] = cfg.gravity.z;
+        c.domain_min[0] = cfg.domain_min.x; c.domain_min[1] = cfg.domain_min.y; c.domain_min[2] = cfg.domain_min.z;
+        c.domain_max[0] = cfg.domain_max.x; c.domain_max[1] = cfg.domain_max.y; c.domain_max[2] = cfg.domain_max.z;
+        c.material_count = std::uint32_t(m);
+        c.materials = mats.data();
+        c.pair_restitution = pair.data();
+        c.rect_wall_count = std::uint32_t(rects.size());
+        c.rect_walls = rects.data();
+        c.line_wall_count = std::uint32_t(lines.size());
+        c.line_walls = lines.data();
+        c.grid_cell_size = cfg.grid_cell_size;
+        c.contact_capacity = cfg.contact_capacity;
+        c.collide_variant = cfg.run.collide_variant == CollideVariant::two_phase ? 1 : 0;
+        c.periodic = cfg.periodic;
+        c.shear_rate = cfg.shear_rate;
+        c.precision = cfg.precision;
+    }
+};
+
+// a ParticleSet's arrays as dem_particles (data(): valid for empty sets too)
+inline dem_particles view(ParticleSet& s) {
+    dem_particles p{};
+    p.count = s.size();
+    p.ids = s.ids.data();
+    p.positions = &s.positions.data()->x;
+    p.velocities = &s.velocities.data()->x;
+    p.angular_velocities = &s.angular_velocities.data()->x;
+    p.radii = s.radii.data();
+    p.masses = s.masses.data();
+    p.material_ids = s.material_ids.data();
+    return p;
+}
+
+// a dem_status as the reference's exception (error.hpp:10-49) with the reference kernel name
+[[noreturn]] inline void rethrow(const dem_ctx* c, int rc) {
+    dem_error e{};
+    dem_last_error(c, &e);
+    static const char* names[] = {"Integrate", "CalcHash", "BitonicSort", "FindCellBoundsAndReorder",
+                                  "ForceGravity", "InitializeContactIDs", "Collide", "CollideRectangle",
+                                  "CollideLine"};
+    const std::string kernel = (e.kernel >= 0 && e.kernel < DEM_KERNEL_COUNT) ? names[e.kernel] : "?";
+    switch (rc) {
+        case DEM_ERR_CONFIG: throw ConfigError(e.message);
+        case DEM_ERR_CAPACITY: throw CapacityError(kernel, e.message, e.particle_slot);
+        case DEM_ERR_DEGENERATE: throw DegenerateContactError("Collide", e.message);
+        case DEM_ERR_KERNEL: throw KernelError(kernel, e.message);
+        case DEM_ERR_ARGUMENT: throw std::invalid_argument(e.message[0] ? e.message : "dem_b200: invalid argument at the C ABI");
+        default: throw DeviceError(e.message);
+    }
+}
+
+}  // namespace detail
+
 class Simulation {
   public:
     Simulation(ParticleSet initial, SimConfig config, int device = 0) : cfg_(std::move(config)) {
@@ -704,81 +786,20 @@ class Simulation {
         self->traces_fresh_ = true;
     }
 
-    static dem_particles view(ParticleSet& s) {
-        dem_particles p{};
-        p.count = s.size();
-        p.ids = s.ids.data();
-        p.positions = &s.positions[0].x;
-        p.velocities = &s.velocities[0].x;
-        p.angular_velocities = &s.angular_velocities[0].x;
-        p.radii = s.radii.data();
-        p.masses = s.masses.data();
-        p.material_ids = s.material_ids.data();
-        return p;
-    }
+    static dem_particles view(ParticleSet& s) { return detail::view(s); }
 
     void build_c_config() {
-        const auto m = cfg_.materials.size();
-        mats_.resize(m);
-        pair_.resize(m * m);
-        for (std::size_t k = 0; k < m; ++k) {
-            const auto& q = cfg_.materials.params(std::uint32_t(k));
-            mats_[k] = dem_material{q.poisson_ratio, q.shear_modulus, q.youngs_modulus, q.restitution, q.sliding_friction};
-        }
-        for (std::size_t a = 0; a < m; ++a)
-            for (std::size_t b = 0; b < m; ++b) pair_[a * m + b] = cfg_.materials.pair_restitution(std::uint32_t(a), std::uint32_t(b));
-        rects_.clear();
-        for (const auto& w : cfg_.rect_walls)
-            rects_.push_back(dem_rect_wall{{w.corner.x, w.corner.y, w.corner.z}, {w.edge_u.x, w.edge_u.y, w.edge_u.z},
-                                           {w.edge_v.x, w.edge_v.y, w.edge_v.z}, w.material_id});
-        lines_.clear();
-        for (const auto& w : cfg_.line_walls)
-            lines_.push_back(dem_line_wall{{w.a.x, w.a.y, w.a.z}, {w.b.x, w.b.y, w.b.z}, w.material_id});
-        ccfg_ = dem_config{};
-        ccfg_.dt = cfg_.dt;
-        ccfg_.gravity[0] = cfg_.gravity.x; ccfg_.gravity[1] = cfg_.gravity.y; ccfg_.gravity[2] = cfg_.gravity.z;
-        ccfg_.domain_min[0] = cfg_.domain_min.x; ccfg_.domain_min[1] = cfg_.domain_min.y; ccfg_.domain_min[2] = cfg_.domain_min.z;
-        ccfg_.domain_max[0] = cfg_.domain_max.x; ccfg_.domain_max[1] = cfg_.domain_max.y; ccfg_.domain_max[2] = cfg_.domain_max.z;
-        ccfg_.material_count = std::uint32_t(m);
-        ccfg_.materials = mats_.data();
-        ccfg_.pair_restitution = pair_.data();
-        ccfg_.rect_wall_count = std::uint32_t(rects_.size());
-        ccfg_.rect_walls = rects_.data();
-        ccfg_.line_wall_count = std::uint32_t(lines_.size());
-        ccfg_.line_walls = lines_.data();
-        ccfg_.grid_cell_size = cfg_.grid_cell_size;
-        ccfg_.contact_capacity = cfg_.contact_capacity;
-        ccfg_.collide_variant = cfg_.run.collide_variant == CollideVariant::two_phase ? 1 : 0;
-        ccfg_.periodic = cfg_.periodic;
-        ccfg_.shear_rate = cfg_.shear_rate;
-        ccfg_.precision = cfg_.precision;
+        cc_.build(cfg_);
+        ccfg_ = cc_.c;
     }
 
     void check(int rc) const { if (rc != DEM_OK) rethrow(ctx_.get(), rc); }
 
-    [[noreturn]] static void rethrow(const dem_ctx* c, int rc) {
-        dem_error e{};
-        dem_last_error(c, &e);
-        static const char* names[] = {"Integrate", "CalcHash", "BitonicSort", "FindCellBoundsAndReorder",
-                                      "ForceGravity", "InitializeContactIDs", "Collide", "CollideRectangle",
-                                      "CollideLine"};
-        const std::string kernel = (e.kernel >= 0 && e.kernel < DEM_KERNEL_COUNT) ? names[e.kernel] : "?";
-        switch (rc) {
-            case DEM_ERR_CONFIG: throw ConfigError(e.message);
-            case DEM_ERR_CAPACITY: throw CapacityError(kernel, e.message, e.particle_slot);
-            case DEM_ERR_DEGENERATE: throw DegenerateContactError("Collide", e.message);
-            case DEM_ERR_KERNEL: throw KernelError(kernel, e.message);
-            case DEM_ERR_ARGUMENT: throw std::invalid_argument(e.message);
-            default: throw DeviceError(e.message);
-        }
-    }
+    [[noreturn]] static void rethrow(const dem_ctx* c, int rc) { detail::rethrow(c, rc); }
 
     SimConfig cfg_;
+    detail::CConfig cc_;
     dem_config ccfg_{};
-    std::vector<dem_material> mats_;
-    std::vector<double> pair_;
-    std::vector<dem_rect_wall> rects_;
-    std::vector<dem_line_wall> lines_;
     std::unique_ptr<dem_ctx, CtxDeleter> ctx_;
     mutable ParticleSet state_;
     mutable ForceAccumulator forces_;

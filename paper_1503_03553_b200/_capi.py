@@ -127,6 +127,15 @@ SIGNATURES = [
     ("dem_ipc_handle", C.c_int, [C.c_int, C.c_void_p, C.c_void_p]),
     ("dem_ipc_open", C.c_int, [C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]),
     ("dem_ipc_close", C.c_int, [C.c_int, C.c_void_p]),
+    # host-free sharded stepping
+    ("dem_create_sharded", C.c_int, [C.POINTER(dem_config), C.POINTER(dem_particles), C.c_int, C.c_int, C.c_int,
+                                     C.POINTER(_P)]),
+    ("dem_shard_info", C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_uint64)]),
+    ("dem_shard_handle", C.c_int, [_P, C.c_void_p]),
+    ("dem_shard_connect", C.c_int, [_P, C.c_void_p]),
+    ("dem_shard_connect_local", C.c_int, [_P, _P, _P]),
+    ("dem_shard_launch", C.c_int, [_P, C.c_int]),
+    ("dem_shard_wait", C.c_int, [_P, C.POINTER(dem_step_metrics)]),
     ("dem_set_contacts", C.c_int, [_P, C.POINTER(C.c_uint32), C.POINTER(C.c_int32), C.POINTER(C.c_double), C.c_int64]),
     ("dem_selftest_division", C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.POINTER(C.c_uint64)]),
 ]

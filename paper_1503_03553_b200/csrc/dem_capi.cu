@@ -3,6 +3,7 @@
 //
 // Host arithmetic that feeds the kernels (grid, per-material-pair tables) is compiled with
 // -ffp-contract=off so it rounds exactly as the reference does (core/CMakeLists.txt:32-37).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -99,6 +100,22 @@ struct dem_ctx {
     uint32_t* h_counters = nullptr;
     size_t tile_pairs = 0, imp_cap = 0, imp_used = 0;
     uint32_t rec_bytes = 0, rec_dt_off = 0, ghost_bytes = 0;
+
+    // host-free sharded stepping (dem_create_sharded): device-resident counts, the
+    // inbox block the neighbours store into, their inboxes, one graph per history parity
+    bool shard = false;
+    int rank = 0, nranks = 1;
+    uint32_t* dn = nullptr;              // [0] phase slots (owned + ghosts), [1] owned slots
+    uint8_t* inbox = nullptr;
+    size_t inbox_bytes = 0;
+    uint64_t cap_rec = 0;                // records per inbox region
+    uint8_t* peer[2] = {nullptr, nullptr};  // lower / upper neighbour's inbox (nullptr: none)
+    bool peer_ipc[2] = {false, false};   // opened with cudaIpcOpenMemHandle (closed at destroy)
+    bool connected = false, primed = false, launched = false;
+    bool stream_wait = true;             // flag waits as stream memory operations (else k_shard_wait)
+    cudaGraphExec_t shard_graph[2] = {nullptr, nullptr};
+    uint64_t launch_pb = 0;
+    int64_t launch_sb = 0;
 
     // asynchronous stepping (dem_step_async): steps launched but not yet collected, and the
     // readback stream that overlaps dem_get_particles with the tail of the last step
@@ -477,6 +494,10 @@ void free_ctx(dem_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->side) cudaStreamSynchronize(c->side);
     for (auto& g : c->graph) if (g) cudaGraphExecDestroy(g);
+    for (auto& g : c->shard_graph) if (g) cudaGraphExecDestroy(g);
+    for (int k = 0; k < 2; ++k)
+        if (c->peer_ipc[k] && c->peer[k] && !(k == 1 && c->peer_ipc[0] && c->peer[0] == c->peer[1]))
+            cudaIpcCloseMemHandle(c->peer[k]);
     for (auto& g : c->graph_async) if (g) cudaGraphExecDestroy(g);
     for (auto& e : c->ev_state) if (e) cudaEventDestroy(e);
     if (c->side) cudaStreamDestroy(c->side);
@@ -872,6 +893,10 @@ int dem_step(dem_ctx* ctx, int nsteps, dem_step_metrics* last) {
     cudaSetDevice(ctx->device);
     SETTLE(ctx);
     REQUIRE_STATE(ctx);
+    if (ctx->shard) {  // host-free sharded steps: every rank's process (or thread) calls this
+        const int rc = dem_shard_launch(ctx, nsteps);
+        return rc != DEM_OK ? rc : dem_shard_wait(ctx, last);
+    }
     if (ctx->n == 0) {
         ctx->step_index += nsteps;
         if (last) { std::memset(last, 0, sizeof(*last)); last->step = ctx->step_index; }
@@ -920,7 +945,6 @@ int dem_force_phase(dem_ctx* ctx, uint32_t flags, dem_step_metrics* m) {
     if (!ctx || (flags & ~static_cast<uint32_t>(DEM_PHASE_STEP))) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
     SETTLE(ctx);
-    REQUIRE_STATE(ctx);
     REQUIRE_STATE(ctx);
     return run_phase(ctx, flags, m, flags == DEM_PHASE_STEP);
 }
@@ -1177,6 +1201,10 @@ int dem_last_error(const dem_ctx* ctx, dem_error* out) {
     return DEM_OK;
 }
 
+namespace {
+int shard_collect(dem_ctx* c, dem_step_metrics* m);  // host-free sharded stepping, below
+}  // namespace
+
 int dem_time_steps(dem_ctx* ctx, int nsteps, size_t flush_bytes, float* step_ms, dem_step_metrics* last) {
     if (!ctx || nsteps < 0 || (nsteps && !step_ms)) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
@@ -1192,15 +1220,23 @@ int dem_time_steps(dem_ctx* ctx, int nsteps, size_t flush_bytes, float* step_ms,
     for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
     const uint64_t pb = ctx->phase_count;
     const int64_t sb = ctx->step_index;
+    if (ctx->shard && (!ctx->primed || ctx->launched)) return DEM_ERR_ARGUMENT;  // dem_step first
+    if (ctx->shard) { ctx->launch_pb = pb; ctx->launch_sb = sb; ctx->launched = true; }
     for (int k = 0; k < nsteps; ++k) {
         if (flush_bytes) launch_flush(ctx->flush_buf, flush_bytes, ctx->stream);
+        CUDA_TRY(cudaEventRecord(ev[2 * k], ctx->stream));
+        if (ctx->shard) {
+            // a sharded step includes the waits for the neighbours' records
+            CUDA_TRY(cudaGraphLaunch(ctx->shard_graph[ctx->shist], ctx->stream));
+            ctx->shist ^= 1;
+        } else {
+            CUDA_TRY(cudaGraphLaunch(ctx->graph[(ctx->phase_count + 1) & 1], ctx->stream));
+        }
         ++ctx->phase_count;
         ++ctx->step_index;
-        CUDA_TRY(cudaEventRecord(ev[2 * k], ctx->stream));
-        CUDA_TRY(cudaGraphLaunch(ctx->graph[ctx->phase_count & 1], ctx->stream));
         CUDA_TRY(cudaEventRecord(ev[2 * k + 1], ctx->stream));
     }
-    int rc = collect(ctx, last, pb, sb, true);
+    int rc = ctx->shard ? shard_collect(ctx, last) : collect(ctx, last, pb, sb, true);
     for (int k = 0; k < nsteps; ++k) cudaEventElapsedTime(&step_ms[k], ev[2 * k], ev[2 * k + 1]);
     for (auto& e : ev) cudaEventDestroy(e);
     return rc;
@@ -1376,7 +1412,7 @@ uint64_t dem_slab_owned(const dem_ctx* ctx) { return ctx && ctx->slab ? ctx->n_o
 
 int dem_slab_migrate(dem_ctx* ctx, int integrate, void* send_lo, void* send_hi, uint64_t cap_records,
                      uint64_t* n_lo, uint64_t* n_hi) {
-    if (!ctx || !ctx->slab || !n_lo || !n_hi) return DEM_ERR_ARGUMENT;
+    if (!ctx || !ctx->slab || ctx->shard || !n_lo || !n_hi) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
     CUDA_TRY(cudaMemsetAsync(ctx->counters, 0, 8 * sizeof(uint32_t), ctx->stream));
     const StepParams p = make_params(ctx, 0);
@@ -1399,7 +1435,7 @@ int dem_slab_migrate(dem_ctx* ctx, int integrate, void* send_lo, void* send_hi, 
 }
 
 int dem_slab_import(dem_ctx* ctx, const void* recs_lo, uint64_t n_lo, const void* recs_hi, uint64_t n_hi) {
-    if (!ctx || !ctx->slab) return DEM_ERR_ARGUMENT;
+    if (!ctx || !ctx->slab || ctx->shard) return DEM_ERR_ARGUMENT;
     if (ctx->n_own + n_lo + n_hi > ctx->n_cap || (ctx->imp_used / ctx->K) + n_lo + n_hi > ctx->imp_cap)
         return set_error(ctx, DEM_ERR_CAPACITY, -1, 0, 0, ctx->step_index, "slab: context capacity exceeded by imports");
     cudaSetDevice(ctx->device);
@@ -1416,7 +1452,7 @@ int dem_slab_import(dem_ctx* ctx, const void* recs_lo, uint64_t n_lo, const void
 }
 
 int dem_slab_halo(dem_ctx* ctx, void* send_lo, void* send_hi, uint64_t cap_records, uint64_t* n_lo, uint64_t* n_hi) {
-    if (!ctx || !ctx->slab || !n_lo || !n_hi) return DEM_ERR_ARGUMENT;
+    if (!ctx || !ctx->slab || ctx->shard || !n_lo || !n_hi) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
     CUDA_TRY(cudaMemsetAsync(ctx->counters, 0, 8 * sizeof(uint32_t), ctx->stream));
     const StepParams p = make_params(ctx, 0);
@@ -1430,7 +1466,7 @@ int dem_slab_halo(dem_ctx* ctx, void* send_lo, void* send_hi, uint64_t cap_recor
 }
 
 int dem_slab_ghosts(dem_ctx* ctx, const void* recs_lo, uint64_t n_lo, const void* recs_hi, uint64_t n_hi) {
-    if (!ctx || !ctx->slab) return DEM_ERR_ARGUMENT;
+    if (!ctx || !ctx->slab || ctx->shard) return DEM_ERR_ARGUMENT;
     if (ctx->n_own + n_lo + n_hi > ctx->n_cap)
         return set_error(ctx, DEM_ERR_CAPACITY, -1, 0, 0, ctx->step_index, "slab: context capacity exceeded by ghosts");
     cudaSetDevice(ctx->device);
@@ -1443,7 +1479,7 @@ int dem_slab_ghosts(dem_ctx* ctx, const void* recs_lo, uint64_t n_lo, const void
 }
 
 int dem_slab_force(dem_ctx* ctx, uint32_t flags, dem_step_metrics* m) {
-    if (!ctx || !ctx->slab) return DEM_ERR_ARGUMENT;
+    if (!ctx || !ctx->slab || ctx->shard) return DEM_ERR_ARGUMENT;
     cudaSetDevice(ctx->device);
     flags = (flags & ~static_cast<uint32_t>(DEM_PHASE_INTEGRATE)) | kPhaseSlab;
     const uint64_t pb = ctx->phase_count;
@@ -1487,6 +1523,355 @@ int dem_ipc_open(int device, const void* handle64, void** ptr) {
 int dem_ipc_close(int device, void* ptr) {
     if (cudaSetDevice(device) != cudaSuccess) return DEM_ERR_CUDA;
     return cudaIpcCloseMemHandle(ptr) == cudaSuccess ? DEM_OK : DEM_ERR_CUDA;
+}
+
+// ---- host-free sharded stepping --------------------------------------
+// dem_create_sharded builds rank `rank` of a z-slab decomposition from the GLOBAL initial set (the
+// same partition on every rank); the caller all-gathers the 64-byte inbox handles
+// (dem_shard_handle) with whatever it has (NCCL, MPI, torch.distributed) and connects
+// (dem_shard_connect), or wires contexts of one process directly (dem_shard_connect_local). Steps
+// then run without the host: record counts stay on the device, neighbours store into each other's
+// inbox blocks and signal with release flags, and each step is one CUDA graph.
+namespace {
+
+using CuWaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+CuWaitFn g_cu_wait = nullptr;
+bool g_cu_wait_probed = false;
+
+CuWaitFn cu_stream_wait() {
+    if (!g_cu_wait_probed) {
+        g_cu_wait_probed = true;
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_cu_wait = reinterpret_cast<CuWaitFn>(fn);
+    }
+    return g_cu_wait;
+}
+
+SlabBufs make_shard(const dem_ctx* c, int hpar) {
+    SlabBufs s = make_slab(c, nullptr, nullptr, c->cap_rec);
+    s.H_old = c->hist[hpar];
+    s.dn = c->dn;
+    s.inbox = c->inbox;
+    s.peer_lo = c->peer[0];
+    s.peer_hi = c->peer[1];
+    s.n_cap = static_cast<uint32_t>(c->n_cap);
+    s.imp_cap = static_cast<uint32_t>(c->imp_cap);
+    return s;
+}
+
+int shard_wait(dem_ctx* c, const SlabBufs& s, uint32_t kind) {
+    if (c->stream_wait) {
+        CuWaitFn w = cu_stream_wait();
+        for (uint32_t side = 0; side < 2; ++side) {
+            if (!c->peer[side]) continue;
+            const CUdeviceptr f = reinterpret_cast<CUdeviceptr>(c->inbox + 4 * (2 * kind + side));
+            if (!w || w(reinterpret_cast<CUstream>(c->stream), f, 1u, CU_STREAM_WAIT_VALUE_EQ) != CUDA_SUCCESS)
+                return DEM_ERR_CUDA;
+        }
+        return DEM_OK;
+    }
+    launch_shard_wait(s, kind, c->stream);
+    return DEM_OK;
+}
+
+// One force phase of the sharded step, history parity hpar (hist[hpar] -> hist[hpar ^ 1]):
+// migrate -> post -> wait -> import -> halo -> post -> wait -> ghosts -> the 7 force-phase kernels
+// over the device-resident slot count.
+int enqueue_shard_phase(dem_ctx* c, bool integrate, uint32_t flags, int hpar) {
+    dem_ctx* const ctx = c;  // CUDA_TRY reports into ctx
+    const SlabBufs s = make_shard(c, hpar);
+    StepParams p = make_params(c, 0);
+    cudaStream_t st = c->stream;
+    CUDA_TRY(cudaMemsetAsync(c->counters, 0, 8 * sizeof(uint32_t), st));
+    launch_shard_migrate(p, s, integrate, st);
+    launch_shard_post(s, 0, st);
+    int rc = shard_wait(c, s, 0);
+    if (rc != DEM_OK) return rc;
+    launch_shard_import(s, st);
+    launch_shard_halo(p, s, st);
+    launch_shard_post(s, 1, st);
+    rc = shard_wait(c, s, 1);
+    if (rc != DEM_OK) return rc;
+    launch_shard_ghosts(s, st);
+    // the force phase: bins Y into X, detects and forces for owned slots; n from dn[0]
+    p = make_params(c, (flags & ~static_cast<uint32_t>(DEM_PHASE_INTEGRATE)) | kPhaseSlab);
+    p.n = static_cast<uint32_t>(c->n_cap);
+    PhaseBufs b = make_bufs(c, 0);
+    b.old_h = c->hist[hpar];
+    b.old_h.pos = c->hrm_pos;
+    b.old_h.cnt = c->hrm_cnt;
+    b.cur_h = c->hist[hpar ^ 1];
+    b.n_tiles_det = detect_tiles(static_cast<uint32_t>(c->n_cap));
+    b.dn = c->dn;
+    launch_phase_begin(p, b, st);
+    launch_integrate_hash(p, b, false, st);
+    launch_scan_cells(p, b, st);
+    launch_scatter(p, b, st);
+    launch_reorder(p, b, st);
+    launch_detect(p, b, st);
+    launch_force_reduce(p, b, st);
+    CUDA_TRY(cudaGetLastError());
+    return DEM_OK;
+}
+
+int build_shard_graphs(dem_ctx* c) {
+    dem_ctx* const ctx = c;  // CUDA_TRY reports into ctx
+    for (int par = 0; par < 2; ++par) {
+        cudaGraphExec_t& ge = c->shard_graph[par];
+        if (ge) { cudaGraphExecDestroy(ge); ge = nullptr; }
+        cudaGraph_t g;
+        CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        const int rc = enqueue_shard_phase(c, true, DEM_PHASE_STEP, par);
+        const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+        if (rc != DEM_OK || e != cudaSuccess) {
+            cudaGetLastError();
+            if (e == cudaSuccess) cudaGraphDestroy(g);
+            return DEM_ERR_CUDA;
+        }
+        const cudaError_t ie = cudaGraphInstantiate(&ge, g, 0);
+        cudaGraphDestroy(g);
+        if (ie != cudaSuccess) { cudaGetLastError(); return DEM_ERR_CUDA; }
+    }
+    return DEM_OK;
+}
+
+// rank r's slab of the global set: whole cell planes along z, balanced by particle count
+// (slab.py's global_grid / cell_planes / slab_bounds, the same arithmetic)
+int shard_partition(const dem_config* cfg, const dem_particles* all, int rank, int nranks, double* h_out,
+                    int32_t* z_lo, int32_t* z_hi, std::vector<uint64_t>* owned, uint64_t* ghosts, uint64_t* cap_rec,
+                    std::string* why) {
+    double r_max = 0.0;
+    for (uint64_t i = 0; i < all->count; ++i) r_max = std::max(r_max, all->radii[i]);
+    dem_grid g{};
+    int rc = make_grid(cfg, r_max, &g, why);
+    if (rc != DEM_OK) return rc;
+    const double ez = cfg->domain_max[2] - cfg->domain_min[2];
+    const double inv_z = (cfg->periodic & 4u) ? 1.0 / (ez / g.nz) : 1.0 / g.cell_size;
+    if (nranks > g.nz) { *why = std::to_string(nranks) + " slabs need at least as many cell planes (grid has " + std::to_string(g.nz) + ")"; return DEM_ERR_CONFIG; }
+    std::vector<int> plane(all->count);
+    std::vector<double> hist(g.nz, 0.0);
+    for (uint64_t i = 0; i < all->count; ++i) {
+        double f = std::floor((all->positions[3 * i + 2] - cfg->domain_min[2]) * inv_z);
+        if (!std::isfinite(f)) f = -1.0;
+        const int z = static_cast<int>(std::min<double>(std::max<double>(f, 0.0), g.nz - 1));
+        plane[i] = z;
+        hist[z] += 1.0;
+    }
+    std::vector<double> cum(g.nz);
+    double acc = 0.0;
+    for (int z = 0; z < g.nz; ++z) cum[z] = (acc += hist[z]);
+    const double total = g.nz ? cum[g.nz - 1] : 0.0;
+    std::vector<int> cuts{0};
+    for (int k = 1; k < nranks; ++k) {
+        const double target = total * k / nranks;
+        int z = static_cast<int>(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin()) + 1;
+        z = std::max(z, cuts.back() + 1);
+        z = std::min(z, g.nz - (nranks - k));
+        cuts.push_back(z);
+    }
+    cuts.push_back(g.nz);
+    // records per inbox region: the same on every rank (the neighbours compute the inbox layout
+    // from their own value): two of the fullest cell planes, at least N / (4 nranks) and 4096
+    double max_plane = 0.0;
+    for (int z = 0; z < g.nz; ++z) max_plane = std::max(max_plane, hist[z]);
+    *cap_rec = std::max<uint64_t>({4096, static_cast<uint64_t>(2.0 * max_plane) + 1024, all->count / (4 * nranks)});
+    *z_lo = cuts[rank];
+    *z_hi = cuts[rank + 1];
+    *h_out = g.cell_size;
+    owned->clear();
+    *ghosts = 0;
+    const bool ring = (cfg->periodic & 4u) != 0;
+    const int below = ring ? (*z_lo - 1 + g.nz) % g.nz : *z_lo - 1, above = ring ? *z_hi % g.nz : *z_hi;
+    for (uint64_t i = 0; i < all->count; ++i) {
+        if (plane[i] >= *z_lo && plane[i] < *z_hi) owned->push_back(i);
+        else if (plane[i] == below || plane[i] == above) ++*ghosts;
+    }
+    return DEM_OK;
+}
+
+int shard_collect(dem_ctx* c, dem_step_metrics* m) {
+    dem_ctx* const ctx = c;  // CUDA_TRY reports into ctx
+    uint32_t dn[2] = {0, 0};
+    CUDA_TRY(cudaMemcpyAsync(c->h_ctl, c->ctl, sizeof(DevCtl), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(dn, c->dn, sizeof(dn), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    CUDA_TRY(cudaGetLastError());
+    c->launched = false;
+    const int rc = collect(c, m, c->launch_pb, c->launch_sb, true, true);
+    c->n = c->n_asm = dn[0];
+    c->n_own = dn[1];
+    return rc;
+}
+
+}  // namespace
+
+int dem_create_sharded(const dem_config* cfg, const dem_particles* all, int device, int rank, int nranks,
+                       dem_ctx** out) {
+    if (!cfg || !all || !out || nranks < 1 || rank < 0 || rank >= nranks) return DEM_ERR_ARGUMENT;
+    *out = nullptr;
+    std::string why;
+    int rc = validate(cfg, all, &why);
+    if (rc == DEM_OK) rc = check_unique_ids(all->ids, all->count, &why);
+    if (rc == DEM_OK && cfg->collide_variant == 0) { why = "sharded contexts run the two_phase collide variant"; rc = DEM_ERR_CONFIG; }
+    double h = 0.0;
+    int32_t z_lo = 0, z_hi = 0;
+    std::vector<uint64_t> idx;
+    uint64_t ghosts = 0, cap_rec = 0;
+    if (rc == DEM_OK) rc = shard_partition(cfg, all, rank, nranks, &h, &z_lo, &z_hi, &idx, &ghosts, &cap_rec, &why);
+    if (rc != DEM_OK) {
+        std::snprintf(g_create_error.message, sizeof(g_create_error.message), "%s", why.c_str());
+        g_create_error.code = rc;
+        return rc;
+    }
+    // the owned subset, then a slab context with the global cell size
+    const uint64_t n = idx.size();
+    std::vector<uint32_t> ids(n), mat(n);
+    std::vector<double> pos(3 * n), vel(3 * n), omg(3 * n), rad(n), mass(n);
+    for (uint64_t k = 0; k < n; ++k) {
+        const uint64_t i = idx[k];
+        ids[k] = all->ids[i];
+        mat[k] = all->material_ids[i];
+        rad[k] = all->radii[i];
+        mass[k] = all->masses[i];
+        for (int a = 0; a < 3; ++a) {
+            pos[3 * k + a] = all->positions[3 * i + a];
+            vel[3 * k + a] = all->velocities[3 * i + a];
+            omg[3 * k + a] = all->angular_velocities[3 * i + a];
+        }
+    }
+    dem_particles owned{n, ids.data(), pos.data(), vel.data(), omg.data(), rad.data(), mass.data(), mat.data()};
+    dem_config scfg = *cfg;
+    scfg.grid_cell_size = h;
+    const uint64_t capacity = 1024 + (3 * (n + ghosts)) / 2;
+    dem_ctx* ctx = nullptr;
+    rc = dem_create_slab(&scfg, &owned, device, z_lo, z_hi, capacity, &ctx);
+    if (rc != DEM_OK) return rc;
+    ctx->shard = true;
+    ctx->rank = rank;
+    ctx->nranks = nranks;
+    ctx->cap_rec = cap_rec;
+    ctx->inbox_bytes = inbox_region(1, 1, ctx->cap_rec, ctx->rec_bytes, ctx->ghost_bytes) + ctx->cap_rec * ctx->ghost_bytes;
+    uint8_t* box = nullptr;
+    cudaError_t e = dalloc(ctx, &box, ctx->inbox_bytes);
+    if (e == cudaSuccess) e = dalloc(ctx, &ctx->dn, 2);
+    if (e == cudaSuccess) {
+        ctx->inbox = box;
+        const uint32_t dn0[2] = {static_cast<uint32_t>(n), static_cast<uint32_t>(n)};
+        e = cudaMemcpyAsync(ctx->dn, dn0, sizeof(dn0), cudaMemcpyHostToDevice, ctx->stream);  // X holds the owned set
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    }
+    if (e != cudaSuccess) {
+        free_ctx(ctx);
+        std::snprintf(g_create_error.message, sizeof(g_create_error.message), "CUDA allocation of the shard inbox failed");
+        g_create_error.code = DEM_ERR_CUDA;
+        return DEM_ERR_CUDA;
+    }
+    *out = ctx;
+    return DEM_OK;
+}
+
+int dem_shard_info(const dem_ctx* ctx, int32_t* z_lo, int32_t* z_hi, uint64_t* owned) {
+    if (!ctx || !ctx->shard) return DEM_ERR_ARGUMENT;
+    if (z_lo) *z_lo = ctx->z_lo;
+    if (z_hi) *z_hi = ctx->z_hi;
+    if (owned) *owned = ctx->n_own ? ctx->n_own : ctx->n;
+    return DEM_OK;
+}
+
+int dem_shard_handle(const dem_ctx* ctx, void* handle64) {
+    if (!ctx || !ctx->shard || !handle64) return DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, ctx->inbox) != cudaSuccess) return DEM_ERR_CUDA;
+    std::memcpy(handle64, &h, sizeof(h));
+    return DEM_OK;
+}
+
+namespace {
+int shard_finish_connect(dem_ctx* ctx) {
+    ctx->connected = true;
+    ctx->stream_wait = cu_stream_wait() != nullptr;
+    if (build_shard_graphs(ctx) != DEM_OK) {  // no stream memory operations in graphs: spin waits
+        ctx->stream_wait = false;
+        CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+        if (build_shard_graphs(ctx) != DEM_OK) return set_error(ctx, DEM_ERR_CUDA, -1, 0, 0, ctx->step_index, "shard graph capture failed");
+    }
+    return DEM_OK;
+}
+}  // namespace
+
+int dem_shard_connect(dem_ctx* ctx, const void* handles) {
+    if (!ctx || !ctx->shard || !handles || ctx->connected) return DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    const bool ring = (ctx->periodic & 4u) != 0;
+    const int R = ctx->nranks, r = ctx->rank;
+    const int nb[2] = {ring || r > 0 ? (r - 1 + R) % R : -1, ring || r < R - 1 ? (r + 1) % R : -1};
+    for (int side = 0; side < 2; ++side) {
+        if (nb[side] < 0) continue;
+        if (nb[side] == r) { ctx->peer[side] = ctx->inbox; continue; }
+        if (side == 1 && nb[1] == nb[0] && ctx->peer_ipc[0]) { ctx->peer[1] = ctx->peer[0]; ctx->peer_ipc[1] = true; continue; }
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, static_cast<const uint8_t*>(handles) + 64 * nb[side], sizeof(h));
+        void* ptr = nullptr;
+        if (cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+            return set_error(ctx, DEM_ERR_CUDA, -1, 0, 0, ctx->step_index,
+                             "shard: cannot open the inbox of rank " + std::to_string(nb[side]) + " (no peer access?)");
+        ctx->peer[side] = static_cast<uint8_t*>(ptr);
+        ctx->peer_ipc[side] = true;
+    }
+    return shard_finish_connect(ctx);
+}
+
+int dem_shard_connect_local(dem_ctx* ctx, dem_ctx* lo, dem_ctx* hi) {
+    if (!ctx || !ctx->shard || ctx->connected) return DEM_ERR_ARGUMENT;
+    if ((lo && !lo->shard) || (hi && !hi->shard)) return DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    for (dem_ctx* o : {lo, hi})
+        if (o && o->device != ctx->device) {
+            const cudaError_t e = cudaDeviceEnablePeerAccess(o->device, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return DEM_ERR_CUDA;
+            cudaGetLastError();
+        }
+    ctx->peer[0] = lo ? lo->inbox : nullptr;
+    ctx->peer[1] = hi ? hi->inbox : nullptr;
+    return shard_finish_connect(ctx);
+}
+
+int dem_shard_launch(dem_ctx* ctx, int nsteps) {
+    if (!ctx || !ctx->shard || !ctx->connected || nsteps < 0 || ctx->launched) return DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    ctx->launch_pb = ctx->phase_count;
+    ctx->launch_sb = ctx->step_index;
+    if (!ctx->primed) {  // the constructor's force-only pass (pipeline.cpp:83), collectively
+        const int rc = enqueue_shard_phase(ctx, false, DEM_PHASE_GRAVITY | DEM_PHASE_PP | DEM_PHASE_RECT | DEM_PHASE_LINE,
+                                           ctx->shist);
+        if (rc != DEM_OK) return rc;
+        ctx->shist ^= 1;
+        ++ctx->phase_count;
+        ctx->primed = true;
+        ctx->launch_pb = ctx->phase_count;
+    }
+    for (int k = 0; k < nsteps; ++k) {
+        CUDA_TRY(cudaGraphLaunch(ctx->shard_graph[ctx->shist], ctx->stream));
+        ctx->shist ^= 1;
+        ++ctx->phase_count;
+        ++ctx->step_index;
+    }
+    ctx->launched = true;
+    return DEM_OK;
+}
+
+int dem_shard_wait(dem_ctx* ctx, dem_step_metrics* last) {
+    if (!ctx || !ctx->shard) return DEM_ERR_ARGUMENT;
+    cudaSetDevice(ctx->device);
+    if (!ctx->launched) {
+        if (last) { std::memset(last, 0, sizeof(*last)); last->step = ctx->step_index; }
+        return DEM_OK;
+    }
+    return shard_collect(ctx, last);
 }
 
 int dem_selftest_division(int device, uint64_t n, uint64_t seed, uint64_t* mismatches) {

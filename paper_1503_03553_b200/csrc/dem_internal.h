@@ -121,6 +121,9 @@ struct PhaseBufs {
     size_t cap;              // pair slots in key/dt (SoA stride of dt)
     uint32_t ft_stride;      // SoA stride of ft (n, or the slab context's slot capacity)
     DevCtl* ctl;
+    // host-free (sharded) phases: the slot count lives in device memory (written by the slab
+    // exchange kernels) and the grids are sized for the capacity; nullptr: StepParams::n
+    const uint32_t* dn;
 };
 
 // Slab decomposition buffers (dem_slab.cu). X: state after the previous force phase (owned and
@@ -143,7 +146,30 @@ struct SlabBufs {
     size_t hcap;             // pair slots in key/dt (SoA stride)
     uint32_t K;
     DevCtl* ctl;
+    // host-free (sharded) stepping: device-resident counts and the inboxes
+    uint32_t* dn;            // [0] slots of the force phase (owned + ghosts) [1] owned slots
+    uint8_t* inbox;          // this rank's inbox block (kInboxHeader + 4 record regions)
+    uint8_t* peer_lo;        // the z-neighbours' inbox blocks (nullptr: no neighbour that side)
+    uint8_t* peer_hi;
+    uint32_t n_cap, imp_cap; // slot capacity, history-import capacity (records)
 };
+
+// Inbox block of a sharded rank: a header (flags[4], counts[4]; index 2 kind + side, kind 0
+// migrants / 1 ghosts, side 0 = from the lower neighbour / 1 = from the upper) and four record
+// regions in that order, cap_send records each. Neighbours store records and counts into it and
+// raise the flag; the owner waits for the flag, consumes, and clears it.
+constexpr size_t kInboxHeader = 256;
+__host__ __device__ inline size_t inbox_region(uint32_t kind, uint32_t side, size_t cap, size_t rec_bytes, size_t ghost_bytes) {
+    const size_t mig = cap * rec_bytes, gh = cap * ghost_bytes;
+    return kInboxHeader + (kind == 0 ? side * mig : 2 * mig + side * gh);
+}
+
+void launch_shard_migrate(const StepParams& p, const SlabBufs& s, bool integrate, cudaStream_t st);
+void launch_shard_post(const SlabBufs& s, uint32_t kind, cudaStream_t st);
+void launch_shard_wait(const SlabBufs& s, uint32_t kind, cudaStream_t st);  // spin fallback of the stream wait
+void launch_shard_import(const SlabBufs& s, cudaStream_t st);
+void launch_shard_halo(const StepParams& p, const SlabBufs& s, cudaStream_t st);
+void launch_shard_ghosts(const SlabBufs& s, cudaStream_t st);
 
 void launch_slab_migrate(const StepParams& p, const SlabBufs& s, bool integrate, cudaStream_t st);
 void launch_slab_import(const SlabBufs& s, const void* recs, uint32_t n, uint32_t base, size_t imp_off, cudaStream_t st);

@@ -432,3 +432,128 @@ def build_local_slabs(ps: ParticleSet, cfg: SimConfig, nranks: int, rank_ids: Se
         capacity = int(1024 + headroom * (len(owned.ids) + ghosts))
         ranks.append(backend(scfg, owned, z_lo, z_hi, capacity, device=device))
     return ranks, bounds, g
+
+
+# ---------------------------------------------------------------------------------------------
+# Host-free sharded stepping (dem_create_sharded): the whole step is one CUDA graph
+# per rank, counts stay on the device, neighbours store records into each other's inboxes.
+
+def _owned_of(lib, ctx, check):
+    """The slab's owned particles, their forces and history rows (halo copies dropped)."""
+    n = int(lib.dem_size(ctx))
+    s = ParticleSet(n)
+    check(lib.dem_get_particles(ctx, C.byref(s.c_struct())))
+    f = np.zeros((n, 3))
+    t = np.zeros((n, 3))
+    check(lib.dem_get_forces(ctx, f.ctypes.data_as(C.POINTER(C.c_double)), t.ctypes.data_as(C.POINTER(C.c_double))))
+    cnt = lib.dem_get_contacts(ctx, None, None, None, 0)
+    o = np.zeros(cnt, np.uint32)
+    p = np.zeros(cnt, np.int32)
+    d = np.zeros((cnt, 3))
+    lib.dem_get_contacts(ctx, o.ctypes.data_as(C.POINTER(C.c_uint32)), p.ctypes.data_as(C.POINTER(C.c_int32)),
+                         d.ctypes.data_as(C.POINTER(C.c_double)), cnt)
+    own = (s.material_ids & GHOST_BIT) == 0
+    ids = s.ids
+    hist_owner = ids[o]
+    hist_key = np.where(p >= 0, ids[np.maximum(p, 0)], p.astype(np.int64) & 0xFFFFFFFF).astype(np.uint32)
+    mine = own[o] if cnt else np.zeros(0, bool)
+    return select(s, own), f[own], t[own], (hist_owner[mine], hist_key[mine], d[mine])
+
+
+class ShardedSimulation:
+    """Rank `rank` of `nranks` of the host-free sharded step. Every rank passes the same GLOBAL
+    initial set; the library keeps this rank's z-slab. Connect with connect_torch (one process per
+    rank, CUDA-IPC inboxes over NVLink) or connect_local (ranks of one process)."""
+
+    def __init__(self, all_particles: ParticleSet, cfg: SimConfig, rank: int, nranks: int, device: int = 0):
+        self.lib = _capi.lib()
+        self.cfg, self.rank, self.nranks, self.device = cfg, rank, nranks, device
+        self._ccfg = _Config(cfg)
+        ps = all_particles.contiguous()
+        ctx = C.c_void_p()
+        rc = self.lib.dem_create_sharded(C.byref(self._ccfg.c), C.byref(ps.c_struct()), device, rank, nranks,
+                                         C.byref(ctx))
+        if rc != 0:
+            _raise(self.lib, None, rc)
+        self.ctx = ctx
+
+    def __del__(self):
+        self.close()
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.dem_destroy(self.ctx)
+            self.ctx = None
+
+    def _check(self, rc):
+        if rc != 0:
+            _raise(self.lib, self.ctx, rc)
+
+    def info(self):
+        lo, hi, n = C.c_int32(), C.c_int32(), C.c_uint64()
+        self._check(self.lib.dem_shard_info(self.ctx, C.byref(lo), C.byref(hi), C.byref(n)))
+        return lo.value, hi.value, n.value
+
+    def handle(self) -> bytes:
+        h = (C.c_char * 64)()
+        self._check(self.lib.dem_shard_handle(self.ctx, h))
+        return bytes(h)
+
+    def connect(self, handles: Sequence[bytes]):
+        buf = (C.c_char * (64 * len(handles))).from_buffer_copy(b"".join(handles))
+        self._check(self.lib.dem_shard_connect(self.ctx, buf))
+
+    def connect_local(self, lo: Optional["ShardedSimulation"], hi: Optional["ShardedSimulation"]):
+        self._check(self.lib.dem_shard_connect_local(self.ctx, lo.ctx if lo else None, hi.ctx if hi else None))
+
+    def launch(self, n: int = 1):
+        self._check(self.lib.dem_shard_launch(self.ctx, n))
+
+    def wait(self) -> StepMetrics:
+        m = _capi.dem_step_metrics()
+        self._check(self.lib.dem_shard_wait(self.ctx, C.byref(m)))
+        return StepMetrics.from_c(m)
+
+    def step(self, n: int = 1) -> StepMetrics:
+        """n graph-launched steps (one rank per process: dem_step = launch + wait)."""
+        m = _capi.dem_step_metrics()
+        self._check(self.lib.dem_step(self.ctx, n, C.byref(m)))
+        return StepMetrics.from_c(m)
+
+    def time_steps(self, nsteps: int, flush_bytes: int = 0):
+        ms = (C.c_float * max(nsteps, 1))()
+        m = _capi.dem_step_metrics()
+        self._check(self.lib.dem_time_steps(self.ctx, nsteps, flush_bytes, ms, C.byref(m)))
+        return [float(ms[k]) for k in range(nsteps)], StepMetrics.from_c(m)
+
+    def size(self) -> int:
+        return int(self.lib.dem_size(self.ctx))
+
+    def owned(self):
+        return _owned_of(self.lib, self.ctx, self._check)
+
+
+def connect_torch(sim: ShardedSimulation, group=None):
+    """All-gather the 64-byte inbox handles over torch.distributed (any backend) and connect."""
+    import torch.distributed as dist
+    allh = [None] * sim.nranks
+    dist.all_gather_object(allh, sim.handle(), group=group)
+    sim.connect(allh)
+
+
+def local_shards(ps: ParticleSet, cfg: SimConfig, nranks: int, device: int = 0) -> List[ShardedSimulation]:
+    """All ranks of one process (one GPU or several with peer access), wired directly."""
+    shards = [ShardedSimulation(ps, cfg, r, nranks, device) for r in range(nranks)]
+    ring = bool(getattr(cfg, "periodic", 0) & 4)
+    for r, sh in enumerate(shards):
+        lo = shards[(r - 1) % nranks] if (ring or r > 0) else None
+        hi = shards[(r + 1) % nranks] if (ring or r < nranks - 1) else None
+        sh.connect_local(lo, hi)
+    return shards
+
+
+def step_local(shards: Sequence[ShardedSimulation], n: int = 1) -> List[StepMetrics]:
+    """n steps of every rank of one process: launch all, then wait for all."""
+    for sh in shards:
+        sh.launch(n)
+    return [sh.wait() for sh in shards]

@@ -29,3 +29,16 @@ def test_cpp_namespace_alias_switch(cuda):
     r = subprocess.run([binp], capture_output=True, text=True, timeout=300)
     print(r.stdout, r.stderr)
     assert r.returncode == 0 and "PASSED" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_cpp_sharded_simulation(cuda):
+    """tests/cpp/shard_test.cpp: the C++ multi-GPU entry point (include/demb200/sharded.hpp over
+    dem_create_sharded / dem_shard_*) for 1-4 ranks, walled and periodic Lees-Edwards, bitwise
+    against one demb200::Simulation — no Python in the loop."""
+    binp = os.path.join(HERE, "cpp", "shard_test")
+    if not os.path.exists(binp):
+        pytest.skip("tests/cpp/shard_test not built")
+    r = subprocess.run([binp], capture_output=True, text=True, timeout=600)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0 and "PASSED" in r.stdout, r.stdout + r.stderr

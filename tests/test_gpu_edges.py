@@ -188,3 +188,44 @@ def test_largest_contact_capacity(cuda, orc, periodic):
     sim = dem.Simulation(ps, cfg)
     m = sim.step()
     assert m.contacts > 0
+
+
+def _poly_pair_state(n_pairs, seed):
+    """Polydisperse two-particle clusters (radius ratio up to 1:2, masses ~ r^3) at centre distance
+    (r_a + r_b)(1 + e) with e = k 2^-52 (k = -4..4) and e = +-2^-41, +-2^-39 (the edges of the
+    sqrt-free classification's 2^-40 band): k_detect's non-monodisperse bounds (MONO = false)."""
+    rng = np.random.default_rng(seed)
+    eps = [k * 2.0 ** -52 for k in range(-4, 5)] + [2.0 ** -41, -(2.0 ** -41), 2.0 ** -39, -(2.0 ** -39)]
+    rows, pid = [], 0
+    for c in range(n_pairs):
+        e = eps[c % len(eps)]
+        ra, rb = 0.005 * rng.uniform(0.5, 1.0), 0.005 * rng.uniform(0.5, 1.0)
+        centre = np.array([0.05 + 0.04 * (c % 10), 0.05 + 0.04 * ((c // 10) % 10), 0.05 + 0.04 * (c // 100)])
+        u = rng.normal(size=3)
+        u /= np.linalg.norm(u)
+        d = (ra + rb) * (1.0 + e)
+        a, b = centre - 0.5 * d * u, centre + 0.5 * d * u
+        rows.append((pid, tuple(a), (0.0, 0.0, 0.0), (0.0, 0.0, 0.0), ra, 1e-3 * (ra / 0.005) ** 3, 0))
+        rows.append((pid + 1, tuple(b), (0.0, 0.0, 0.0), (0.0, 0.0, 0.0), rb, 1e-3 * (rb / 0.005) ** 3, 0))
+        pid += 2
+    return dem.ParticleSet.from_lists(rows)
+
+
+def test_contact_boundary_ulps_polydisperse(cuda, orc):
+    """The polydisperse classification path (per-candidate reach and bounds) decides pairs around
+    the contact boundary exactly as the reference: the priming pass (positions exactly as built)
+    and two steps bitwise against the CPU restatement."""
+    from oracle.oracle import OracleSim
+    ps = _poly_pair_state(520, 11)
+    cfg = basic_config(0.5)
+    sim = dem.Simulation(ps, cfg)
+    osim = OracleSim(orc, ps, cfg)
+    o, _, _ = sim.contacts()
+    n_prime = len(o)
+    assert n_prime == len(osim.history())
+    assert 0 < n_prime < 2 * 520  # some pairs touch, some do not
+    _compare(sim, osim)
+    for _ in range(2):
+        m, om = sim.step(), osim.step()
+        assert (m.contacts, m.pp_contact_events) == (om.contacts, om.pp_contact_events)
+        _compare(sim, osim)

@@ -643,7 +643,7 @@ class Simulation {
         last_.clamps = m.clamps;
         last_.friction_max_ratio = m.friction_max_ratio;
         last_.capped_contacts = m.capped_contacts;
-        if (record && record_traces_) {  // pipeline.cpp:356-362
+        if (record && record_traces_ && !cfg_.periodic) {  // pipeline.cpp:356-362 (no traces in periodic boxes)
             const WarpReport r = model_report(traces(), cfg_.warp);
             last_.model_cycles_baseline = r.cycles_baseline;
             last_.model_cycles_two_phase = r.cycles_two_phase;

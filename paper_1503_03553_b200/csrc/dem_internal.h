@@ -177,7 +177,10 @@ void launch_slab_halo(const StepParams& p, const SlabBufs& s, uint32_t n_own, cu
 void launch_slab_ghosts(const SlabBufs& s, const void* recs, uint32_t n, uint32_t base, bool from_hi, cudaStream_t st);
 
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 16;
+#ifndef DEM_SCAN_ITEMS
+#define DEM_SCAN_ITEMS 16
+#endif
+constexpr int kScanItems = DEM_SCAN_ITEMS;  // cells per thread of k_scan_cells (tile = 256 x this)
 constexpr int kDetectThreads = 256;  // 8 warps; a detection tile is one warp (32 slots)
 
 inline uint32_t scan_tiles(uint32_t M) { return (M + kScanThreads * kScanItems - 1) / (kScanThreads * kScanItems); }

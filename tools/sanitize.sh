@@ -4,7 +4,7 @@
 mkdir -p gpurun_out
 : > gpurun_out/sanitize_summary.txt
 for tool in memcheck racecheck synccheck; do
-  for mode in ${MODES:-walled periodic fp32 slab}; do
+  for mode in ${MODES:-walled periodic fp32 slab shard_local}; do
     log=gpurun_out/sanitize_${tool}_${mode}.log
     extra=""
     [ $tool = memcheck ] && extra="--leak-check full"

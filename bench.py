@@ -462,7 +462,7 @@ def run_b200(args):
     force_ach = nbytes["k_force_reduce"] / (kms["k_force_reduce"] * 1e-3) / 1e9
     dom_ach = nbytes[dom] / (kms[dom] * 1e-3) / 1e9
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r02_traffic.json")
     if os.path.exists(tpath):
         try:
             traffic = json.load(open(tpath)).get(dom)
@@ -471,7 +471,7 @@ def run_b200(args):
     # what actually bounds the dominant kernel (FP64 pipe / latency, not HBM): the ncu capture
     # of the same workload committed under profiles/ (tools/profile_round.sh)
     util = None
-    upath = os.path.join(ROOT, "profiles", "r01_kernel_util.json")
+    upath = os.path.join(ROOT, "profiles", "r02_kernel_util.json")
     if os.path.exists(upath):
         try:
             util = json.load(open(upath)).get(dom)
@@ -532,7 +532,7 @@ def run_b200(args):
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_ach, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": dom_ach / peak,
                      "traffic": traffic, "algorithmic_bytes": nbytes[dom], "ms": kms[dom],
-                     "ncu": dict(util, source="profiles/r01_kernel_util.json (ncu --set full)") if util else None},
+                     "ncu": dict(util, source="profiles/r02_kernel_util.json (ncu --set full)") if util else None},
         "force_kernel": {"name": "k_force_reduce", "achieved": force_ach, "frac": force_ach / peak, "ms": kms["k_force_reduce"],
                          "algorithmic_bytes": nbytes["k_force_reduce"]},
         "kernel_ms": kms,

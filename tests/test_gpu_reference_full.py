@@ -147,3 +147,70 @@ def test_config0_1000_steps_statistics_vs_reference(cuda, ref):
     assert np.all(rel <= 1e-9)
     assert cb == cr
     assert abs(kr[-1] - 0.17712) < 5e-5  # KE_end printed 1.7712e-01 J
+
+
+@pytest.mark.parametrize("case", ["configs1_262144", "configs2_1M_poly_friction"])
+def test_fp32_mode_priming_pass_vs_reference(cuda, ref, case):
+    """north_star's fp32 bar against the LIVE reference (not only against the GPU's own fp64 path):
+    the fp32 throughput mode's priming pass on identical inputs at BASELINE.json's full sizes.
+    * Contact-pair sets are identical (detection stays the exact fp64 classification).
+    * Forces within 1e-5 and torques within 1e-5 r of the particle's sum of contact-term
+      magnitudes (Hertz k_n dn^1.5 + spring k_t |delta_t| + damping eta |v_rel|, the scale of
+      tests/test_fp32_mode.py): an fp32 evaluation is accurate relative to the terms it sums, and
+      in the configs[2] stress case (spins up to 50 rad/s) a separating contact's elastic and
+      damping terms cancel to 1/400 of their size, so 1e-5 of the net |F| would ask fp32 for
+      ~4e-8 relative accuracy per term. The error relative to sum |F_k| is printed alongside.
+    * New tangential displacements (delta_t = v_t dt in the priming pass) within 1e-5 relative to
+      |delta_t| + |v_rel| dt, |v_rel| <= |v_i - v_j| + |w_i| r_i + |w_j| r_j."""
+    dem = cuda
+    from oracle.oracle import Oracle, OracleSim, RefSim
+    from test_fp32_mode import contact_scale
+    if case == "configs1_262144":
+        ps, dmax = dem.gen_packing(262144, s=1.8, jit=0.2, poly=False, seed=1)
+        cfg = dem.packing_config(dmax)
+    else:
+        ps, dmax = dem.gen_packing(1 << 20, s=1.4, jit=0.2, poly=True, seed=3, omega_half=50.0)
+        cfg = dem.packing_config(dmax, poly=True)
+    rsim = RefSim(ref, ps, cfg)
+    osim = OracleSim(Oracle(), ps, cfg)
+    cfg.precision = 1
+    sim = dem.Simulation(ps, cfg)
+    a, r, o = sim.particles(), rsim.state(), osim.state()
+    ia, ir, io = np.argsort(a.ids), np.argsort(r.ids), np.argsort(o.ids)
+    assert np.array_equal(a.ids[ia], r.ids[ir]) and np.array_equal(a.ids[ia], o.ids[io])
+    fa, ta = sim.forces().force[ia], sim.forces().torque[ia]
+    fr, tr = (x[ir] for x in rsim.forces())
+    co, cp, cd = sim.contacts()
+    scale = contact_scale(a, co, cp, cd)[ia]
+    has = scale > 0
+    ef = np.linalg.norm(fa - fr, axis=1)
+    et = np.linalg.norm(ta - tr, axis=1)
+    rad = a.radii[ia]
+    fs = np.maximum(osim.force_scale()[0][io], 1e-300)
+    print(f"{case}: fp32 vs reference: force {np.max(ef[has] / scale[has]):.2e}, torque "
+          f"{np.max(et[has] / (scale[has] * rad[has])):.2e} of the contact-term sums; force "
+          f"{np.max(np.abs(fa - fr).max(1) / fs):.2e} of sum |F_k|")
+    assert np.all(ef[~has] == 0.0) and np.all(et[~has] == 0.0)
+    assert np.all(ef[has] <= 1e-5 * scale[has]) and np.all(et[has] <= 1e-5 * scale[has] * rad[has])
+    ro, rp, rt, rd = rsim.table()
+    ko, kp = _pairs(co, cp, a.ids)
+    ro2, rp2 = _pairs(ro[rt], rp[rt], r.ids)
+    kb, kr = np.stack([ko, kp], 1), np.stack([ro2, rp2], 1)
+    ob, orr = np.lexsort((kb[:, 1], kb[:, 0])), np.lexsort((kr[:, 1], kr[:, 0]))
+    assert len(kb) == len(kr) and np.array_equal(kb[ob], kr[orr]), "contact sets differ"
+    # |v_rel| bound per contact, from the reference state by stable id (walls: partner terms 0)
+    pos_of = np.empty(int(r.ids.max()) + 1, dtype=np.int64)
+    pos_of[r.ids] = np.arange(len(r.ids))
+    oi = pos_of[kb[ob][:, 0]]
+    pj = kb[ob][:, 1]
+    wall = pj < 0
+    ji = pos_of[np.where(wall, r.ids[0], pj)]
+    v, w, rr = r.velocities, r.angular_velocities, r.radii
+    vrel = (np.linalg.norm(v[oi] - np.where(wall[:, None], 0.0, v[ji]), axis=1)
+            + np.linalg.norm(w[oi], axis=1) * rr[oi]
+            + np.where(wall, 0.0, np.linalg.norm(w[ji], axis=1) * rr[ji]))
+    db, dr = cd[ob], rd[rt][orr]
+    sd = np.linalg.norm(dr, axis=1) + vrel * cfg.dt
+    ed = np.max(np.linalg.norm(db - dr, axis=1) / np.maximum(sd, 1e-300))
+    print(f"{case}: fp32 vs reference: delta_t {ed:.2e}")
+    assert ed <= 1e-5

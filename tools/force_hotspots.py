@@ -1,0 +1,76 @@
+"""k_force_reduce<false,false,false> hot spots by code region: executed warp instructions, stall
+samples, lane efficiency, L1 shared wavefronts and global / local sectors, from an ncu source page
+(SASS) and nvdisasm line info. Regions are line ranges of csrc/dem_kernels.cu and dem_math.cuh.
+
+usage: python tools/force_hotspots.py <ncu sass csv> <nvdisasm --print-line-info output>
+"""
+import collections
+import csv
+import re
+import sys
+
+sys.path.insert(0, __file__.rsplit("/", 1)[0])
+from sass_lines import line_map  # noqa: E402
+
+K = [  # (file, first line, last line, region) — dem_kernels.cu as of this round
+    ("dem_kernels.cu", 895, 957, "pair entries + partner / history prefetch"),
+    ("dem_kernels.cu", 970, 996, "history match"),
+    ("dem_kernels.cu", 1007, 1102, "contact body (owner/partner state, table, memo)"),
+    ("dem_kernels.cu", 1103, 1155, "FastMath flag / exact fallback"),
+    ("dem_kernels.cu", 1232, 1300, "unit setup + phase A (owner staging)"),
+    ("dem_kernels.cu", 1301, 1347, "phase B loop (gathers at chunk start, F/T and history stores)"),
+    ("dem_kernels.cu", 1348, 1374, "phase C (owner sums in list order)"),
+    ("dem_kernels.cu", 1375, 1460, "tail (F, T out, metrics)"),
+    ("dem_math.cuh", 15, 65, "math: vector ops"),
+    ("dem_math.cuh", 120, 200, "math: FastMath sqrt / reciprocal / division"),
+    ("dem_math.cuh", 200, 275, "math: geometry, coefficients, force, cap"),
+]
+
+
+def region(loc):
+    f, ln = loc
+    for kf, a, b, name in K:
+        if f == kf and a <= ln <= b:
+            return name
+    return "other: " + f
+
+
+def main():
+    csv_path, dis_path = sys.argv[1:3]
+    dis = open(dis_path).read()
+    fn = re.search(r"\.text\.(\S*k_force_reduceILb0ELb0ELb0E\S*)", dis).group(1)
+    lm = line_map(dis_path, fn)
+    rows = list(csv.reader(open(csv_path)))
+    hdr = rows[1]
+    col = {c: hdr.index(c) for c in ["Instructions Executed", "Thread Instructions Executed",
+                                      "Warp Stall Sampling (All Samples)", "L1 Wavefronts Shared",
+                                      "L2 Theoretical Sectors Global", "L2 Theoretical Sectors Local"]}
+    body = [r for r in rows[2:] if r and r[0].startswith("0x")]
+    base = int(body[0][0], 16)
+    agg = collections.defaultdict(lambda: collections.Counter())
+    for r in body:
+        off = int(r[0], 16) - base
+        loc, _ = lm.get(off, (("?", 0), ""))
+        g = agg[region(loc)]
+        for c, i in col.items():
+            g[c] += int(float(r[i] or 0))
+    tot = collections.Counter()
+    for g in agg.values():
+        tot.update(g)
+    print("| region | warp insts % | stall samples % | lanes / inst | shared wavefronts % | global sectors % | local sectors |")
+    print("|---|---|---|---|---|---|---|")
+    for name, g in sorted(agg.items(), key=lambda kv: -kv[1]["Instructions Executed"]):
+        e = g["Instructions Executed"]
+        print(f"| {name} | {100 * e / tot['Instructions Executed']:.1f} | "
+              f"{100 * g['Warp Stall Sampling (All Samples)'] / tot['Warp Stall Sampling (All Samples)']:.1f} | "
+              f"{g['Thread Instructions Executed'] / max(e, 1):.1f} | "
+              f"{100 * g['L1 Wavefronts Shared'] / max(tot['L1 Wavefronts Shared'], 1):.1f} | "
+              f"{100 * g['L2 Theoretical Sectors Global'] / max(tot['L2 Theoretical Sectors Global'], 1):.1f} | "
+              f"{g['L2 Theoretical Sectors Local']} |")
+    print(f"\ntotals (all captured launches): {tot['Instructions Executed']:.4g} warp insts, "
+          f"{tot['L1 Wavefronts Shared']:.4g} shared wavefronts, {tot['L2 Theoretical Sectors Global']:.4g} "
+          f"global sectors, {tot['L2 Theoretical Sectors Local']:.4g} local sectors")
+
+
+if __name__ == "__main__":
+    main()

@@ -376,6 +376,28 @@ def north_star_sharded(args, world, rank, local):
             "l2": "inputs larger than L2, no flush"}
 
 
+def config3_block(args):
+    """BASELINE configs[3] on this one GPU — 8,388,608 spheres in the periodic Lees-Edwards shear
+    box, the workload of the N > 1 lines — so the scaling curve has its own N = 1 point (the
+    headline `value` stays configs[1]). Single context (the sharded step is bitwise the same)."""
+    import paper_1503_03553_b200 as dem
+    ps, L = dem.gen_periodic_packing(N_CONFIG3, s=1.8, jit=0.2, seed=4)
+    sim = dem.Simulation(ps, dem.periodic_config(L, shear_rate=1.0), device=0)
+    del ps
+    steps = max(3, min(args.steps, 10))
+    for _ in range(3):
+        sim.step()
+    with ClockSampler(0) as clk:
+        step_ms, m = sim.time_steps(steps, 0)
+    total_s = sum(step_ms) / 1e3
+    del sim
+    return {"workload": "8,388,608 spheres, periodic box with Lees-Edwards shear (configs[3]), one GPU",
+            "generator": "G_periodic(8388608, s=1.8, jit=0.2, mono, seed=4), shear rate 1/s", "dtype": "f64",
+            "value": N_CONFIG3 * steps / total_s, "unit": UNIT, "steps": steps, "warmup": 3,
+            "ms_per_step": 1e3 * total_s / steps, "contacts_per_step": int(m.contacts), "clocks": clk.summary(),
+            "l2": "inputs larger than L2, no flush (as the N > 1 lines)"}
+
+
 def north_star_block(args):
     """north_star's target workload on this one GPU: 32M dense frictional spheres (G(33554432,
     s=1.8, jit=0.2, mono, seed=5), mu = 0.3, K = 16), fp64, its own warm-up / timed steps (CUDA
@@ -540,6 +562,7 @@ def run_b200(args):
     }
     del sim
     if world == 1 and not args.no_north_star:
+        line["configs3_1gpu"] = config3_block(args)
         line["north_star_32m"] = north_star_block(args)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:

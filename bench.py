@@ -48,15 +48,18 @@ def peaks():
 
 
 def algorithmic_bytes(n, c, m):
-    """Compulsory bytes per launch of each kernel (d64); see DESIGN.md §4 for the derivation."""
+    """Compulsory bytes per launch of each kernel (d64) in the steady stepping state, where the
+    previous force kernel pre-integrated the state: k_integrate_hash only
+    hashes (reads 32 B of position, writes key + arrival rank), k_force_reduce also writes the
+    96 B/particle pre-integrated state."""
     return {
         "k_phase_begin": 0,
-        "k_integrate_hash": 252 * n,
+        "k_integrate_hash": 40 * n,
         "k_scan_cells": 12 * m,
         "k_scatter": 24 * n,
         "k_reorder": 252 * n,
         "k_detect": 60 * n + 4 * m + 8 * c,
-        "k_force_reduce": 172 * n + 64 * c,
+        "k_force_reduce": 268 * n + 64 * c,
     }
 
 

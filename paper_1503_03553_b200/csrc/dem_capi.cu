@@ -56,6 +56,7 @@ struct dem_ctx {
 
     // device memory
     StateBuf state[2]{};
+    StateBuf pre{};  // single context: the force kernel's pre-integrated state (DevCtl::preint_phase)
     HistBuf hist[2]{};
     double* ft = nullptr;
     uint32_t *key = nullptr, *skey = nullptr, *loc = nullptr, *cnt = nullptr, *cstart = nullptr;
@@ -319,6 +320,7 @@ StepParams make_params(const dem_ctx* c, uint32_t flags) {
     p.shear_rate = c->shear_rate;
     p.shear_u = c->shear_rate * p.Ly;
     if (c->precision == 1) p.flags |= kPhaseFp32;
+    if (!c->slab) p.flags |= kPhasePreint;
     if (c->periodic && (!(c->periodic & 1u) || c->grid.nx >= 5) && (!(c->periodic & 2u) || c->grid.ny >= 5) &&
         (!(c->periodic & 4u) || c->grid.nz >= 5))
         p.flags |= kPhaseInterior;
@@ -337,6 +339,7 @@ PhaseBufs make_bufs(const dem_ctx* c, uint64_t phase) {
     b.old_h = c->hist[prev];
     b.cur_h = c->hist[cur];
     b.ft = c->ft;
+    b.pre = c->pre;
     b.key = c->key; b.skey = c->skey; b.loc = c->loc; b.cnt = c->cnt; b.cstart = c->cstart;
     b.tmp_src = c->tmp_src; b.tmp_id = c->tmp_id; b.prev_slot = c->prev_slot; b.prev_row = c->prev_row;
     b.pair_i = c->pair_i; b.pair_j = c->pair_j;
@@ -447,6 +450,8 @@ int collect(dem_ctx* ctx, dem_step_metrics* m, uint64_t phase_before, int64_t st
         clean.err_key = kNoError;
         for (auto& s : clean.err_sid) s = kNoError;
         clean.halted = 0;
+        clean.preint_phase = ~0ull;  // the failed phase's state is what the caller inspects
+        clean.deferred[0] = clean.deferred[1] = ~0ull;
         CUDA_TRY(cudaMemcpyAsync(ctx->ctl, &clean, sizeof(DevCtl), cudaMemcpyHostToDevice, ctx->stream));
         CUDA_TRY(cudaStreamSynchronize(ctx->stream));
         return code;
@@ -534,6 +539,11 @@ int allocate(dem_ctx* ctx) {
         CUDA_TRY(dalloc(ctx, &ctx->hist[b].cnt, n));
         CUDA_TRY(dalloc(ctx, &ctx->hist[b].key, ctx->cap));
         CUDA_TRY(dalloc(ctx, &ctx->hist[b].dt, 3 * ctx->cap));
+    }
+    if (!ctx->slab) {
+        CUDA_TRY(dalloc(ctx, &ctx->pre.pos_r, n));
+        CUDA_TRY(dalloc(ctx, &ctx->pre.vel_m, n));
+        CUDA_TRY(dalloc(ctx, &ctx->pre.omg, n));
     }
     CUDA_TRY(dalloc(ctx, &ctx->ft, 6 * n));
     CUDA_TRY(dalloc(ctx, &ctx->key, n));
@@ -679,6 +689,7 @@ int upload_state(dem_ctx* ctx, const dem_particles* p, int buf) {
     // sends the ids through the exact host check.
     CUDA_TRY(cudaMemsetAsync(&ctx->ctl->bad_upload, 0xff, sizeof(unsigned long long), s));
     CUDA_TRY(cudaMemsetAsync(&ctx->ctl->maybe_dup, 0, sizeof(unsigned int), s));
+    CUDA_TRY(cudaMemsetAsync(&ctx->ctl->preint_phase, 0xff, sizeof(unsigned long long), s));  // new state
     if (r.ids) CUDA_TRY(cudaMemsetAsync(ctx->idmap, 0, (static_cast<size_t>(ctx->idmask) + 1) / 8, s));
     const PackCheck chk{ctx->ctl, static_cast<uint32_t>(ctx->materials.size()), r.ids ? ctx->idmap : nullptr, ctx->idmask};
     launch_pack_state(ctx->state[buf], r, static_cast<uint32_t>(n), true, s, &chk,
@@ -801,6 +812,8 @@ int dem_create(const dem_config* cfg, const dem_particles* particles, int device
         DevCtl init{};
         init.err_key = kNoError;
         for (auto& s : init.err_sid) s = kNoError;
+        init.preint_phase = ~0ull;
+        init.deferred[0] = init.deferred[1] = ~0ull;
         // on the context's stream: a legacy cudaMemcpy from pageable memory may complete its DMA after
         // later work on this non-blocking stream (upload_state's check-word reset)
         if (cudaMemcpyAsync(ctx->ctl, &init, sizeof(DevCtl), cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
@@ -869,6 +882,8 @@ int dem_clone(const dem_ctx* src, dem_ctx** out) {
         copy(ctx->pair_i, src->pair_i, src->cap * sizeof(uint32_t));
         copy(ctx->pair_j, src->pair_j, src->cap * sizeof(uint32_t));
         copy(ctx->ctl, src->ctl, sizeof(DevCtl));
+        if (rc == DEM_OK && cudaMemsetAsync(&ctx->ctl->preint_phase, 0xff, sizeof(unsigned long long), ctx->stream) != cudaSuccess)
+            rc = DEM_ERR_CUDA;  // the pre-integrated state is not copied: the clone integrates from its state
         copy(ctx->d_pairs, src->d_pairs, kMaxMaterials * kMaxMaterials * sizeof(MatPairH));
         copy(ctx->d_rects, src->d_rects, kMaxWalls * sizeof(RectW));
         copy(ctx->d_lines, src->d_lines, kMaxWalls * sizeof(LineW));
@@ -1039,6 +1054,7 @@ int dem_set_forces(dem_ctx* ctx, const double* force, const double* torque) {
     CUDA_TRY(cudaMemcpyAsync(f, force, 3 * n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     CUDA_TRY(cudaMemcpyAsync(t, torque, 3 * n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     launch_ft_layout(ctx->ft, static_cast<uint32_t>(fs), f, t, static_cast<uint32_t>(n), false, ctx->stream);
+    CUDA_TRY(cudaMemsetAsync(&ctx->ctl->preint_phase, 0xff, sizeof(unsigned long long), ctx->stream));  // new forces
     CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     CUDA_TRY(cudaGetLastError());
     return DEM_OK;
@@ -1384,6 +1400,8 @@ int dem_create_slab(const dem_config* cfg, const dem_particles* owned, int devic
         DevCtl init{};
         init.err_key = kNoError;
         for (auto& s : init.err_sid) s = kNoError;
+        init.preint_phase = ~0ull;
+        init.deferred[0] = init.deferred[1] = ~0ull;
         // on the context's stream: a legacy cudaMemcpy from pageable memory may complete its DMA after
         // later work on this non-blocking stream (upload_state's check-word reset)
         if (cudaMemcpyAsync(ctx->ctl, &init, sizeof(DevCtl), cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||

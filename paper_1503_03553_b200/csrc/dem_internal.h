@@ -17,6 +17,7 @@ constexpr unsigned long long kNoError = ~0ull;
 constexpr uint32_t kPhaseSlab = 64u;  // internal phase flag: slab context (ghost-aware kernels)
 constexpr uint32_t kPhaseInterior = 128u;  // internal: every periodic axis has >= 5 cells (k_detect)
 constexpr uint32_t kPhaseFp32 = 256u;      // internal: fp32 throughput mode (k_force_reduce)
+constexpr uint32_t kPhasePreint = 512u;    // internal: single context; k_force_reduce pre-integrates (PhaseBufs::pre)
 
 struct MatPairH {  // host mirror of MatPair (dem_math.cuh)
     double shear_sum, young_sum, alpha, mu;
@@ -79,6 +80,13 @@ struct DevCtl {
     double le_delta;                            // Lees-Edwards image offset of the upper box
     unsigned long long bad_upload;              // (slot<<8)|reason of the first invalid uploaded particle, atomicMin
     unsigned int maybe_dup;                     // an uploaded id hashed onto an occupied idmap bit
+    // Pre-integration (single context): the force kernel of phase `preint_phase` wrote the next
+    // Integrate's result (its state advanced with the forces it just computed) into PhaseBufs::pre;
+    // the next phase uses it when it integrates and preint_phase == phase - 1 (~0: invalid; every
+    // host-side change of state or forces invalidates it). A non-finite force seen there is the next
+    // Integrate's KernelError, deferred to that phase: deferred[q & 1] = min (slot<<32)|id of phase q.
+    unsigned long long preint_phase;
+    unsigned long long deferred[2];
 };
 
 // Structure-of-arrays particle state for one buffer (sorted slot order).
@@ -102,6 +110,7 @@ struct HistBuf {
 
 struct PhaseBufs {
     StateBuf src, dst;       // reorder gathers src -> dst
+    StateBuf pre;            // single context: pos_r / vel_m / omg pre-integrated by k_force_reduce (src slot order)
     HistBuf old_h, cur_h;    // history of previous phase / written this phase
     double* ft;              // 6 * n (fx|fy|fz|tx|ty|tz), per slot
     uint32_t* key;           // n: cell key per (pre-sort) slot, later sorted keys

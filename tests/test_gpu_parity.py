@@ -181,6 +181,31 @@ def test_nonfinite_force_raises_integrate(cuda):
     assert "non-finite force" in str(e.value)
 
 
+def test_nonfinite_force_from_the_force_phase_raises_next_integrate(cuda):
+    """A force phase that itself produces non-finite forces (two touching particles at +-1e308 m/s:
+    the relative velocity overflows) completes; the NEXT step's Integrate raises KernelError
+    (pipeline.cpp:35-38), as the reference would. On the B200 path the force kernel pre-integrates
+    the next Integrate and defers the error to it; a clone, whose first step
+    integrates from its state, must report the same error (kernel, particle)."""
+    dem = cuda
+    cfg = basic_config(box_for(64))
+    ps = random_dense_state(64, 3)
+    ps.velocities[:] = 0.0
+    a, b = 10, 11  # neighbours in the lattice: make them overlap, then give them opposite huge speeds
+    ps.positions[b] = ps.positions[a] + np.array([ps.radii[a] + ps.radii[b] - 1e-4, 0.0, 0.0])
+    ps.velocities[a, 0], ps.velocities[b, 0] = 1e308, -1e308
+    sim = dem.Simulation(ps, cfg)  # the priming pass computes the non-finite forces without error
+    f = sim.forces().force
+    assert not np.all(np.isfinite(f))
+    twin = sim.clone()
+    with pytest.raises(dem.KernelError) as e1:
+        sim.step()
+    with pytest.raises(dem.KernelError) as e2:
+        twin.step()
+    assert e1.value.kernel == e2.value.kernel == "Integrate"
+    assert str(e1.value) == str(e2.value) and "non-finite force" in str(e1.value)
+
+
 @pytest.mark.parametrize("seed", [7, 8])
 def test_single_loop_variant_bitwise_equals_two_phase(cuda, seed):
     """test_pipeline.cpp:191-220 on the GPU: Alg. 1 (single loop, set_collide_variant(baseline))

@@ -13,14 +13,16 @@ sys.path.insert(0, __file__.rsplit("/", 1)[0])
 from sass_lines import line_map  # noqa: E402
 
 K = [  # (file, first line, last line, region) — dem_kernels.cu as of this round
-    ("dem_kernels.cu", 895, 957, "pair entries + partner / history prefetch"),
-    ("dem_kernels.cu", 970, 996, "history match"),
-    ("dem_kernels.cu", 1007, 1102, "contact body (owner/partner state, table, memo)"),
-    ("dem_kernels.cu", 1103, 1155, "FastMath flag / exact fallback"),
-    ("dem_kernels.cu", 1232, 1300, "unit setup + phase A (owner staging)"),
-    ("dem_kernels.cu", 1301, 1347, "phase B loop (gathers at chunk start, F/T and history stores)"),
-    ("dem_kernels.cu", 1348, 1374, "phase C (owner sums in list order)"),
-    ("dem_kernels.cu", 1375, 1460, "tail (F, T out, metrics)"),
+    ("dem_kernels.cu", 926, 1000, "pair entries + partner / history prefetch"),
+    ("dem_kernels.cu", 1001, 1027, "history match"),
+    ("dem_kernels.cu", 1028, 1044, "pre-integration (next step's Integrate)"),
+    ("dem_kernels.cu", 1055, 1150, "contact body (owner/partner state, table, memo)"),
+    ("dem_kernels.cu", 1151, 1203, "FastMath flag / exact fallback"),
+    ("dem_kernels.cu", 1281, 1353, "unit setup + phase A (owner staging)"),
+    ("dem_kernels.cu", 1354, 1400, "phase B loop (gathers at chunk start, F/T and history stores)"),
+    ("dem_kernels.cu", 1401, 1427, "phase C (owner sums in list order)"),
+    ("dem_kernels.cu", 1428, 1520, "tail (F, T out, metrics)"),
+    ("dem_kernels.cu", 173, 190, "pre-integration (next step's Integrate)"),
     ("dem_math.cuh", 15, 65, "math: vector ops"),
     ("dem_math.cuh", 120, 200, "math: FastMath sqrt / reciprocal / division"),
     ("dem_math.cuh", 200, 275, "math: geometry, coefficients, force, cap"),

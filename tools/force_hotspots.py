@@ -13,15 +13,15 @@ sys.path.insert(0, __file__.rsplit("/", 1)[0])
 from sass_lines import line_map  # noqa: E402
 
 K = [  # (file, first line, last line, region) — dem_kernels.cu as of this round
-    ("dem_kernels.cu", 926, 1000, "pair entries + partner / history prefetch"),
-    ("dem_kernels.cu", 1001, 1027, "history match"),
-    ("dem_kernels.cu", 1028, 1044, "pre-integration (next step's Integrate)"),
-    ("dem_kernels.cu", 1055, 1150, "contact body (owner/partner state, table, memo)"),
-    ("dem_kernels.cu", 1151, 1203, "FastMath flag / exact fallback"),
-    ("dem_kernels.cu", 1281, 1353, "unit setup + phase A (owner staging)"),
-    ("dem_kernels.cu", 1354, 1400, "phase B loop (gathers at chunk start, F/T and history stores)"),
-    ("dem_kernels.cu", 1401, 1427, "phase C (owner sums in list order)"),
-    ("dem_kernels.cu", 1428, 1520, "tail (F, T out, metrics)"),
+    ("dem_kernels.cu", 936, 1011, "pair entries + partner / history prefetch"),
+    ("dem_kernels.cu", 1012, 1038, "history match"),
+    ("dem_kernels.cu", 1039, 1054, "pre-integration (next step's Integrate)"),
+    ("dem_kernels.cu", 1066, 1160, "contact body (partner state, table, memo)"),
+    ("dem_kernels.cu", 1161, 1225, "FastMath flag / exact fallback"),
+    ("dem_kernels.cu", 1306, 1378, "unit setup + phase A (owner staging)"),
+    ("dem_kernels.cu", 1379, 1432, "phase B loop (gathers and owner state at chunk start, F/T and history stores)"),
+    ("dem_kernels.cu", 1433, 1459, "phase C (owner sums in list order)"),
+    ("dem_kernels.cu", 1460, 1560, "tail (F, T out, metrics)"),
     ("dem_kernels.cu", 173, 190, "pre-integration (next step's Integrate)"),
     ("dem_math.cuh", 15, 65, "math: vector ops"),
     ("dem_math.cuh", 120, 200, "math: FastMath sqrt / reciprocal / division"),

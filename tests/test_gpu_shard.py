@@ -143,3 +143,46 @@ def test_shard_ipc_processes_bitwise(cuda, world, kind):
     ps, cfg = _case(dem, kind)
     s1, f1, t1, h1 = single_run(dem, ps, cfg, steps)
     _assert_same(parts, s1, f1, t1, h1)
+
+
+def _hist_sorted(owner, key, d):
+    k = (owner.astype(np.uint64) << np.uint64(32)) | key.astype(np.uint64)
+    o = np.argsort(k, kind="stable")
+    return k[o], bits(d[o])
+
+
+def test_shard_configs3_full_size_bitwise(cuda):
+    """configs[3] at its full size — 8,388,608 spheres in the periodic Lees-Edwards box — over 4
+    sharded ranks (one process, peer pointers) against one context, 4 steps: positions, velocities,
+    forces, torques and every tangential history bitwise equal by stable id."""
+    dem = cuda
+    from paper_1503_03553_b200.slab import local_shards, step_local
+    ps, L = dem.gen_periodic_packing(1 << 23, s=1.8, jit=0.2, seed=4)
+    cfg = dem.periodic_config(L, shear_rate=1.0)
+    steps = 4
+    sim = dem.Simulation(ps, cfg)
+    sim.steps(steps)
+    s1 = sim.particles()
+    fa = sim.forces()
+    o, p, d = sim.contacts()
+    k1 = np.where(p >= 0, s1.ids[np.maximum(p, 0)], p.astype(np.int64) & 0xFFFFFFFF).astype(np.uint32)
+    h1 = _hist_sorted(s1.ids[o], k1, d)
+    a1 = by_id(s1.ids, s1.ids, s1.positions, s1.velocities, fa.force, fa.torque)
+    del sim, o, p, d, k1
+    shards = local_shards(ps, cfg, 4)
+    del ps
+    step_local(shards, 3)
+    step_local(shards, steps - 3)
+    parts = [sh.owned() for sh in shards]
+    for sh in shards:
+        sh.close()
+    ids = np.concatenate([q[0].ids for q in parts])
+    a2 = by_id(ids, ids, np.concatenate([q[0].positions for q in parts]),
+               np.concatenate([q[0].velocities for q in parts]), np.concatenate([q[1] for q in parts]),
+               np.concatenate([q[2] for q in parts]))
+    assert np.array_equal(a1[0], a2[0])
+    for x, y in zip(a1[1:], a2[1:]):
+        assert bitwise_equal(x, y)
+    h2 = _hist_sorted(np.concatenate([q[3][0] for q in parts]), np.concatenate([q[3][1] for q in parts]),
+                      np.concatenate([q[3][2] for q in parts]))
+    assert np.array_equal(h1[0], h2[0]) and np.array_equal(h1[1], h2[1])

@@ -190,7 +190,12 @@ constexpr int kScanThreads = 256;
 #define DEM_SCAN_ITEMS 16
 #endif
 constexpr int kScanItems = DEM_SCAN_ITEMS;  // cells per thread of k_scan_cells (tile = 256 x this)
-constexpr int kDetectThreads = 256;  // 8 warps; a detection tile is one warp (32 slots)
+#ifndef DEM_DET_THREADS
+#define DEM_DET_THREADS 128
+#endif
+// 4 warps per block (8: polydisperse detection 37 us slower at configs[2] — a block's slots free
+// only when its slowest tile is done); a detection tile is one warp (32 slots)
+constexpr int kDetectThreads = DEM_DET_THREADS;
 
 inline uint32_t scan_tiles(uint32_t M) { return (M + kScanThreads * kScanItems - 1) / (kScanThreads * kScanItems); }
 // warp tiles launched (a multiple of the warps per block)

@@ -34,7 +34,8 @@ for name in (sys.argv[1:] or ["mono", "poly"]):
     prof = [sim.profile_step(512 << 20) for _ in range(10)]
     k = {nm: statistics.mean(p.device_kernel_ms[i] for p in prof) for i, nm in enumerate(names)}
     step_ms, _ = sim.time_steps(40, 512 << 20)
+    bin_ = " ".join(f"{nm[2:]} {1e3 * k[nm]:.2f}" for nm in names if nm not in ("k_force_reduce", "k_detect"))
     out.append(f"{name}: force {1e3 * k['k_force_reduce']:.2f} detect {1e3 * k['k_detect']:.2f} "
-               f"step {1e3 * statistics.mean(step_ms):.2f} us")
+               f"step {1e3 * statistics.mean(step_ms):.2f} us" + (f" [{bin_}]" if os.environ.get("AB_ALL") else ""))
     del sim
 print(" | ".join(out))

@@ -3,7 +3,8 @@ ticks in ~1-2 µs steps, so a median of a few steps cannot separate close varian
 of 40 graph-captured steps (L2 flushed before each) and the mean per-kernel event times of 10
 profiled steps, per workload:
   mono  configs[1], 262,144 dense, fp64      fp32  the same in the fp32 mode
-  poly  configs[2], 1,048,576 polydisperse   le    1,048,576 periodic Lees-Edwards box"""
+  poly  configs[2], 1,048,576 polydisperse   le    1,048,576 periodic Lees-Edwards box
+  sX    8,388,608 walled dense pack at spacing X (e.g. s2.0)"""
 import os
 import statistics
 import sys
@@ -16,6 +17,9 @@ def case(name):
     if name == "poly":
         ps, dmax = dem.gen_packing(1 << 20, s=1.4, jit=0.2, poly=True, seed=3, omega_half=50.0)
         return ps, dem.packing_config(dmax, poly=True)
+    if name.startswith("s") and name[1:].replace(".", "").isdigit():  # e.g. s2.0: 8M walled pack at that spacing
+        ps, dmax = dem.gen_packing(1 << 23, s=float(name[1:]), jit=0.2, seed=5)
+        return ps, dem.packing_config(dmax)
     if name == "le":
         ps, L = dem.gen_periodic_packing(1 << 20, s=1.8, jit=0.2, seed=4)
         return ps, dem.periodic_config(L, shear_rate=1.0)

@@ -55,9 +55,10 @@ def test_empty_set(cuda, orc):
     assert sim.forces().force.shape == (0, 3)
 
 
-@pytest.mark.parametrize("n", [1, 33, 1000])
+@pytest.mark.parametrize("n", [1, 33, 129, 160, 1000, 4097])
 def test_ragged_counts_bitwise(cuda, orc, n):
-    """1 particle (free fall), and counts that leave the last tile partly empty."""
+    """1 particle (free fall), and counts that leave the last 32-slot tile partly empty or the last
+    4-tile detection block with one tile (129, 160, 4097)."""
     from oracle.oracle import OracleSim
     cfg = basic_config(box_for(n))
     cfg.gravity = (0.0, 0.0, -9.81)

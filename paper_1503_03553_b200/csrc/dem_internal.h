@@ -199,6 +199,19 @@ constexpr int kDetectThreads = DEM_DET_THREADS;
 
 inline uint32_t scan_tiles(uint32_t M) { return (M + kScanThreads * kScanItems - 1) / (kScanThreads * kScanItems); }
 // warp tiles launched (a multiple of the warps per block)
+// k_detect's per-thread shared-memory list: the fp32 prefilter's kept candidates (up to
+// detect_pass_cap; more sends the lane to the one-stage walk), then its contacts compacted in
+// place (<= K + 1), plus one scratch entry; odd stride, so the lanes' appends are conflict-free.
+// The prefilter keeps the contacts and the pairs within ~2^-18 relative of touching, so K + 8
+// entries leave room; the smaller rows let more detection blocks share an SM when K is large
+// (configs[2], K = 32: detection -13 %; DEM_PF_CAP_EXTRA < 0: 2K, the earlier sizing).
+#ifndef DEM_PF_CAP_EXTRA
+#define DEM_PF_CAP_EXTRA 8
+#endif
+__host__ __device__ inline uint32_t detect_pass_cap(uint32_t K) {
+    return DEM_PF_CAP_EXTRA < 0 ? 2u * K : K + static_cast<uint32_t>(DEM_PF_CAP_EXTRA);
+}
+__host__ __device__ inline uint32_t detect_row_stride(uint32_t K) { return (detect_pass_cap(K) + 1u) | 1u; }
 inline uint32_t detect_tiles(uint32_t n) { return ((n + kDetectThreads - 1) / kDetectThreads) * (kDetectThreads / 32); }
 
 // Launchers (dem_kernels.cu). Each enqueues exactly one kernel on `s`.

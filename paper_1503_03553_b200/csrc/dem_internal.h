@@ -202,11 +202,13 @@ inline uint32_t scan_tiles(uint32_t M) { return (M + kScanThreads * kScanItems -
 // k_detect's per-thread shared-memory list: the fp32 prefilter's kept candidates (up to
 // detect_pass_cap; more sends the lane to the one-stage walk), then its contacts compacted in
 // place (<= K + 1), plus one scratch entry; odd stride, so the lanes' appends are conflict-free.
-// The prefilter keeps the contacts and the pairs within ~2^-18 relative of touching, so K + 8
-// entries leave room; the smaller rows let more detection blocks share an SM when K is large
-// (configs[2], K = 32: detection -13 %; DEM_PF_CAP_EXTRA < 0: 2K, the earlier sizing).
+// The prefilter keeps the contacts and the pairs within ~2^-18 relative of touching, so K
+// entries hold every list short of a CapacityError (a lane with more survivors takes the exact
+// one-stage walk, which also counts an overflow exactly); the smaller rows let more detection
+// blocks share an SM and leave more L1 (profiles/r02_force_variants.md: configs[2] detection
+// -17 %, configs[1] -4 %; DEM_PF_CAP_EXTRA < 0: 2K, the earlier sizing).
 #ifndef DEM_PF_CAP_EXTRA
-#define DEM_PF_CAP_EXTRA 8
+#define DEM_PF_CAP_EXTRA 0
 #endif
 __host__ __device__ inline uint32_t detect_pass_cap(uint32_t K) {
     return DEM_PF_CAP_EXTRA < 0 ? 2u * K : K + static_cast<uint32_t>(DEM_PF_CAP_EXTRA);

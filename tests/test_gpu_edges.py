@@ -131,6 +131,50 @@ def test_capacity_exactly_full_and_one_over(cuda, orc, k_neighbours, ok):
         assert eo.value.code == 3
 
 
+def _icosahedron_cluster(rel):
+    """A centre sphere and 12 neighbours at the icosahedron's vertices, neighbour q at distance
+    reach (1 + rel[q]) from the centre, the neighbours 1.05 reach apart from each other."""
+    r = 0.005
+    c = np.array([0.05, 0.05, 0.05])
+    g = (1 + 5 ** 0.5) / 2
+    verts = [(0, 1, g), (0, -1, g), (0, 1, -g), (0, -1, -g), (1, g, 0), (-1, g, 0), (1, -g, 0), (-1, -g, 0),
+             (g, 0, 1), (-g, 0, 1), (g, 0, -1), (-g, 0, -1)]
+    rows = [(0, tuple(c), (0.0, 0.0, 0.0), (0.0, 0.0, 0.0), r, 1e-3, 0)]
+    for q, (v, e) in enumerate(zip(verts, rel)):
+        u = np.array(v, float) / np.linalg.norm(v)
+        rows.append((q + 1, tuple(c + 2 * r * (1.0 + e) * u), (0.0, 0.0, 0.0), (0.0, 0.0, 0.0), r, 1e-3, 0))
+    return dem.ParticleSet.from_lists(rows)
+
+
+@pytest.mark.parametrize("n_touch,ok", [(3, True), (5, False)])
+def test_prefilter_overflow_takes_exact_walk(cuda, orc, n_touch, ok):
+    """The centre has 12 fp32-prefilter survivors against a kept-list capacity of K = 4: n_touch
+    neighbours overlap it and the other 12 - n_touch sit at reach (1 + 1e-7 .. 1e-6), inside the
+    prefilter's conservative bound but outside the reference's d2 screen (reach2 (1 + 1e-9),
+    pipeline.cpp:144-149). The detection lane falls back to the exact one-stage walk, which finds
+    the reference's contacts (forces bitwise) or raises its CapacityError (5 screen passers > 4)."""
+    from oracle.oracle import OracleSim, OracleError
+    rel = [-(6 - q) * 2.0 ** -44 for q in range(n_touch)] + [(q + 1) * 1e-7 for q in range(12 - n_touch)]
+    ps = _icosahedron_cluster(rel)
+    cfg = basic_config(0.1)
+    cfg.contact_capacity = 4
+    if ok:
+        sim = dem.Simulation(ps, cfg)
+        osim = OracleSim(orc, ps, cfg)
+        for _ in range(3):
+            m, om = sim.step(), osim.step()
+            assert (m.contacts, m.max_contacts_per_particle) == (om.contacts, om.max_contacts_per_particle)
+        assert m.max_contacts_per_particle == n_touch
+        _compare(sim, osim)
+    else:
+        with pytest.raises(dem.CapacityError) as e:
+            dem.Simulation(ps, cfg)
+        assert e.value.kernel == "Collide"
+        with pytest.raises(OracleError) as eo:
+            OracleSim(orc, ps, cfg)
+        assert eo.value.code == 3
+
+
 def test_set_particles_validates_on_device(cuda):
     """dem_set_particles validates every uploaded particle (ParticleSet::validate,
     particle_set.cpp:40-58, plus unique ids below the wall keys): a rejected upload raises

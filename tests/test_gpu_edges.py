@@ -131,32 +131,43 @@ def test_capacity_exactly_full_and_one_over(cuda, orc, k_neighbours, ok):
         assert eo.value.code == 3
 
 
-def _icosahedron_cluster(rel):
+def _icosahedron_cluster(rel, centre=(0.05, 0.05, 0.05), box=None):
     """A centre sphere and 12 neighbours at the icosahedron's vertices, neighbour q at distance
-    reach (1 + rel[q]) from the centre, the neighbours 1.05 reach apart from each other."""
+    reach (1 + rel[q]) from the centre, the neighbours 1.05 reach apart from each other
+    (positions wrapped into [0, box) for a periodic box)."""
     r = 0.005
-    c = np.array([0.05, 0.05, 0.05])
+    c = np.array(centre, float)
     g = (1 + 5 ** 0.5) / 2
     verts = [(0, 1, g), (0, -1, g), (0, 1, -g), (0, -1, -g), (1, g, 0), (-1, g, 0), (1, -g, 0), (-1, -g, 0),
              (g, 0, 1), (-g, 0, 1), (g, 0, -1), (-g, 0, -1)]
     rows = [(0, tuple(c), (0.0, 0.0, 0.0), (0.0, 0.0, 0.0), r, 1e-3, 0)]
     for q, (v, e) in enumerate(zip(verts, rel)):
         u = np.array(v, float) / np.linalg.norm(v)
-        rows.append((q + 1, tuple(c + 2 * r * (1.0 + e) * u), (0.0, 0.0, 0.0), (0.0, 0.0, 0.0), r, 1e-3, 0))
+        x = c + 2 * r * (1.0 + e) * u
+        if box is not None:
+            x = np.mod(x, box)
+        rows.append((q + 1, tuple(x), (0.0, 0.0, 0.0), (0.0, 0.0, 0.0), r, 1e-3, 0))
     return dem.ParticleSet.from_lists(rows)
 
 
+@pytest.mark.parametrize("periodic", [False, True])
 @pytest.mark.parametrize("n_touch,ok", [(3, True), (5, False)])
-def test_prefilter_overflow_takes_exact_walk(cuda, orc, n_touch, ok):
+def test_prefilter_overflow_takes_exact_walk(cuda, orc, n_touch, ok, periodic):
     """The centre has 12 fp32-prefilter survivors against a kept-list capacity of K = 4: n_touch
     neighbours overlap it and the other 12 - n_touch sit at reach (1 + 1e-7 .. 1e-6), inside the
     prefilter's conservative bound but outside the reference's d2 screen (reach2 (1 + 1e-9),
     pipeline.cpp:144-149). The detection lane falls back to the exact one-stage walk, which finds
-    the reference's contacts (forces bitwise) or raises its CapacityError (5 screen passers > 4)."""
+    the reference's contacts (forces bitwise) or raises its CapacityError (5 screen passers > 4).
+    Periodic: the cluster straddles the corner of a periodic box, so the centre's warp takes the
+    wrapped (minimum-image) walk and its fallback."""
     from oracle.oracle import OracleSim, OracleError
     rel = [-(6 - q) * 2.0 ** -44 for q in range(n_touch)] + [(q + 1) * 1e-7 for q in range(12 - n_touch)]
-    ps = _icosahedron_cluster(rel)
-    cfg = basic_config(0.1)
+    if periodic:
+        ps = _icosahedron_cluster(rel, centre=(0.001, 0.002, 0.003), box=0.1)
+        cfg = dem.periodic_config(0.1)
+    else:
+        ps = _icosahedron_cluster(rel)
+        cfg = basic_config(0.1)
     cfg.contact_capacity = 4
     if ok:
         sim = dem.Simulation(ps, cfg)

@@ -1,6 +1,6 @@
 """k_force_reduce<false,false,false> hot spots by code region: executed warp instructions, stall
 samples, lane efficiency, L1 shared wavefronts and global / local sectors, from an ncu source page
-(SASS) and nvdisasm line info. Regions are line ranges of csrc/dem_kernels.cu and dem_math.cuh.
+(SASS) and nvdisasm line info. Regions are marker-delimited line ranges of csrc/dem_kernels.cu and dem_math.cuh (ANCHORS).
 
 usage: python tools/force_hotspots.py <ncu sass csv> <nvdisasm --print-line-info output>
 """
@@ -12,21 +12,53 @@ import sys
 sys.path.insert(0, __file__.rsplit("/", 1)[0])
 from sass_lines import line_map  # noqa: E402
 
-K = [  # (file, first line, last line, region) — dem_kernels.cu as of this round
-    ("dem_kernels.cu", 936, 1011, "pair entries + partner / history prefetch"),
-    ("dem_kernels.cu", 1012, 1038, "history match"),
-    ("dem_kernels.cu", 1039, 1054, "pre-integration (next step's Integrate)"),
-    ("dem_kernels.cu", 1066, 1160, "contact body (partner state, table, memo)"),
-    ("dem_kernels.cu", 1161, 1225, "FastMath flag / exact fallback"),
-    ("dem_kernels.cu", 1306, 1378, "unit setup + phase A (owner staging)"),
-    ("dem_kernels.cu", 1379, 1432, "phase B loop (gathers and owner state at chunk start, F/T and history stores)"),
-    ("dem_kernels.cu", 1433, 1459, "phase C (owner sums in list order)"),
-    ("dem_kernels.cu", 1460, 1560, "tail (F, T out, metrics)"),
-    ("dem_kernels.cu", 173, 190, "pre-integration (next step's Integrate)"),
-    ("dem_math.cuh", 15, 65, "math: vector ops"),
-    ("dem_math.cuh", 120, 200, "math: FastMath sqrt / reciprocal / division"),
-    ("dem_math.cuh", 200, 275, "math: geometry, coefficients, force, cap"),
+SRC = __file__.rsplit("/", 2)[0] + "/paper_1503_03553_b200/csrc/"
+# Regions as (file, start marker, end marker, name): each spans the lines from the first line
+# containing its start marker up to (not including) the first later line containing its end
+# marker, resolved against the current sources so the tool survives edits.
+ANCHORS = [
+    ("dem_kernels.cu", "__device__ __forceinline__ void integrate_particle(", "// the previous force kernel's pre-integrated",
+     "pre-integration (next step's Integrate)"),
+    ("dem_kernels.cu", "struct PairIdx {", "// The force kernel's shared-memory material table",
+     "pair entries + partner / history prefetch"),
+    ("dem_kernels.cu", "// The owner's previous history row entry", "// Pre-integration (single context",
+     "history match"),
+    ("dem_kernels.cu", "// Pre-integration (single context", "struct WarpMetrics {",
+     "pre-integration (next step's Integrate)"),
+    ("dem_kernels.cu", "// One contact of an owner (pi, vi, wi", "#ifndef DEM_FR_FAST",
+     "contact body (partner state, table, memo)"),
+    ("dem_kernels.cu", "#ifndef DEM_FR_FAST", "// The owner-major schedule of a unit",
+     "FastMath flag / exact fallback"),
+    ("dem_kernels.cu", "// The owner-major schedule of a unit", "__device__ __forceinline__ void force_reduce_tile(",
+     "owner-major schedule"),
+    ("dem_kernels.cu", "__device__ __forceinline__ void force_reduce_tile(", "// ---- B: lane = contact",
+     "unit setup + phase A (owner staging)"),
+    ("dem_kernels.cu", "// ---- B: lane = contact", "// ---- C: lane = owner",
+     "phase B loop (gathers and owner state at chunk start, F/T and history stores)"),
+    ("dem_kernels.cu", "// ---- C: lane = owner", "// metrics (pipeline.cpp:338-363)",
+     "phase C (owner sums in list order)"),
+    ("dem_kernels.cu", "// metrics (pipeline.cpp:338-363)", "// One contact of owner i with a history row",
+     "tail (F, T out, metrics)"),
+    ("dem_math.cuh", "struct V3 {", "// 256-bit global accesses", "math: vector ops"),
+    ("dem_math.cuh", "// 256-bit global accesses", "// ---- fp64 divisions sharing one reciprocal",
+     "256-bit loads / stores, x86 conversion"),
+    ("dem_math.cuh", "// ---- fp64 divisions sharing one reciprocal", "struct MatPair {",
+     "math: FastMath sqrt / reciprocal / division"),
+    ("dem_math.cuh", "struct MatPair {", None, "math: geometry, coefficients, force, cap"),
 ]
+
+
+def resolve():
+    out = []
+    for f, a, b, name in ANCHORS:
+        lines = open(SRC + f).read().split("\n")
+        start = next(k for k, l in enumerate(lines) if a in l) + 1
+        end = len(lines) + 1 if b is None else next(k for k, l in enumerate(lines) if k + 1 > start and b in l) + 1
+        out.append((f, start, end - 1, name))
+    return out
+
+
+K = resolve()
 
 
 def region(loc):
